@@ -1,0 +1,161 @@
+/*
+ * liblj.h -- C ABI of the B200 (sm_100a) Lennard-Jones force hot path of
+ * Watanabe & Nakagawa, arXiv 1806.05713.  Implemented by
+ * paper_1806_05713_b200/liblj.so (hand-written CUDA, fp64, no tensor cores).
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers owned by the caller unless stated; the
+ *    library allocates nothing on the device (workspaces are caller-provided)
+ *    and keeps no global device state.
+ *  - q, p: n records of 4 doubles (x, y, z, pad) -- the paper's "AoS with
+ *    padding" layout (Fig. aos4).  Base address 32-byte
+ *    aligned (checked: one 256-bit load per record).  The pad is never read
+ *    into arithmetic and is preserved by every call.
+ *  - Lists are the paper's sorted list (Fig. sorted_list) in
+ *    CSR form, local to a row range [row_begin, row_end): row r <-> atom
+ *    row_begin + r; number_of_partners[rows] (int32), pointer[rows+1] (int64,
+ *    pointer[0] = 0), sorted_list[pointer[rows]] (int32 global atom indices,
+ *    ascending within a row).  n < 2^31 is checked.
+ *  - Full list (half = 0): row i holds every j != i with r_ij^2 < rs^2.
+ *    Half list (half = 1): row i holds only j > i (each pair once, PAPER.md
+ *    Alg. calcforce_sortedlist); a half list must cover all rows [0, n).
+ *  - Geometry: L > 0 is a periodic cube of side L (minimum image, DESIGN.md
+ *    reading C-3); L == 0 is open space (force/energy only).  0 < rc < rs.
+ *  - Stream-ordered and asynchronous on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream), except lj_build_list, which
+ *    synchronises `stream` once to read the entry count.
+ *  - Errors: arguments are validated before anything is enqueued; a failure
+ *    returns LJ_ERR_ARG and launches nothing.  A CUDA launch error returns
+ *    LJ_ERR_CUDA; lj_last_error() gives the detail (thread-local).  Faults of
+ *    already-enqueued kernels surface at the next synchronising call.  No
+ *    exception or abort crosses the ABI.
+ *  - Re-entrant on different streams with disjoint outputs.
+ */
+#ifndef LIBLJ_H
+#define LIBLJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LJ_OK = 0,
+    LJ_ERR_ARG = 1,          /* invalid argument; nothing launched */
+    LJ_ERR_CAPACITY = 2,     /* list capacity too small; *n_entries = required */
+    LJ_ERR_CUDA = 3,         /* CUDA runtime error; see lj_last_error() */
+    LJ_ERR_UNSUPPORTED = 4   /* valid but unsupported combination */
+} lj_status;
+
+/* L: periodic box side (0 = open); rc: cutoff ("simple
+ * truncation", interact iff r^2 < rc^2); rs: search length of the Verlet list
+ * ("register each pair within a search length r_s"). */
+typedef struct {
+    double L;
+    double rc;
+    double rs;
+} lj_geom;
+
+/* ---- layout (§8(a) a1) --------------------------------------------------- */
+
+/* xyz: n x 3 doubles (device) -> out: n x 4 doubles, pad = 0. */
+lj_status lj_pack_aos4(const double *xyz, double *out, int64_t n, void *stream);
+/* in: n x 4 -> xyz: n x 3 (drops the pad). */
+lj_status lj_unpack_aos4(const double *in, double *xyz, int64_t n, void *stream);
+
+/* ---- neighbour list (§8(a) a2-a4) ---------------------- */
+
+/* Bytes of device workspace lj_build_list / lj_cell_order need for n atoms. */
+lj_status lj_build_list_workspace(int64_t n, lj_geom g, size_t *bytes);
+
+/* Linked-cell Verlet list: cells of side L/nc, nc =
+ * floor(L/rs) >= 3 (requires L > 0); cell of an atom from its position wrapped
+ * into [0,L); pairs accepted iff the minimum-image r^2 = (dx*dx + dy*dy) + dz*dz,
+ * evaluated without FMA, is < rs*rs (bit-identical to the oracle's test).
+ * Rows [row_begin, row_end) are built; half = 1 needs the full range.
+ * Outputs number_of_partners[rows], pointer[rows+1], sorted_list[capacity].
+ * *n_entries (HOST) receives the required entry count.  If capacity is too
+ * small the call returns LJ_ERR_CAPACITY (list contents undefined; capacity 0
+ * is a size query).  Synchronises `stream` once. */
+lj_status lj_build_list(const double *q, int64_t n, lj_geom g, int half,
+                        int64_t row_begin, int64_t row_end,
+                        int32_t *number_of_partners, int64_t *pointer,
+                        int32_t *sorted_list, int64_t capacity, int64_t *n_entries,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* Spatial reordering (BASELINE.json config 3): perm[new] = old, the stable
+ * sort of the atoms by cell id (cx*nc + cy)*nc + cz (same cells as the list). */
+lj_status lj_cell_order(const double *q, int64_t n, lj_geom g, int64_t *perm,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* out[k] = in[perm[k]] for n records of 4 doubles (in != out). */
+lj_status lj_permute_rows(const double *in, double *out, const int64_t *perm, int64_t n, void *stream);
+
+/* ---- force (§8(a) a5/a6; PAPER.md Alg. lj_force + Alg. calcforce_sortedlist) */
+
+/* One force step: for every own row i and every j in its row with
+ * r^2 < rc^2: df = (48 - 24 r^6) dt / r^14, p_i -= df r_vec,
+ * and for a half list also p_j += df r_vec (Newton 3; PAPER.md:172 prints
+ * "-", reading C-1).  r_vec = minimum-image q_j - q_i.
+ * Full list: only p of own rows changes, deterministic, no atomics.
+ * Half list: p of any atom changes (fp64 atomics; summation order not
+ * deterministic).  p is indexed by global atom index. */
+lj_status lj_force_step(const double *q, double *p, int64_t n, lj_geom g, double dt, int half,
+                        int64_t row_begin, int64_t row_end,
+                        const int32_t *number_of_partners, const int64_t *pointer,
+                        const int32_t *sorted_list, void *stream);
+
+/* Tuning / instrumentation variant of lj_force_step.
+ * lanes_per_row: 0 = library default, else one of 1,2,4,8,16,32 threads
+ * cooperating on a row.  n_interactions: NULL or a device uint64 to which the
+ * number of list entries inside r_c is ADDED (pair interactions; a full list
+ * counts each pair twice).  ordered != 0 (full list only): one thread per row,
+ * ascending j, the oracle's exact expression order (Alg. 3 accumulating into
+ * the loaded p_i, IEEE division, no FMA) -- bit-identical to the oracle. */
+lj_status lj_force_step_ex(const double *q, double *p, int64_t n, lj_geom g, double dt, int half,
+                           int64_t row_begin, int64_t row_end,
+                           const int32_t *number_of_partners, const int64_t *pointer,
+                           const int32_t *sorted_list, int lanes_per_row, int ordered,
+                           unsigned long long *n_interactions, void *stream);
+
+/* ---- integration and bookkeeping (§8(a) a7, a9) --------------------------- */
+
+/* Drift q_i += p_i dt for atoms [begin, end) (mass 1), bit-identical to the
+ * oracle (no FMA).  Positions are not wrapped. */
+lj_status lj_integrate(double *q, const double *p, int64_t begin, int64_t end, double dt, void *stream);
+
+/* Wrap q into [0,L) (x -= L floor(x/L); x -= L if x >= L) for atoms [0,n) and,
+ * if q_ref != NULL, copy the wrapped records to q_ref (the bookkeeping
+ * reference of PAPER.md:190-192). */
+lj_status lj_wrap(double *q, double *q_ref, int64_t n, double L, void *stream);
+
+/* *out (device double) = max_{i in [begin,end)} |q_i - q_ref_i| (Euclidean). */
+lj_status lj_max_displacement(const double *q, const double *q_ref, int64_t begin, int64_t end,
+                              double *out, void *stream);
+
+/* ---- energy (§8(a) a10; PAPER.md:146 Eq. lj with V(r_c) = 0) -------------- */
+
+/* out (device, 2 doubles) = {KE over own rows, PE over the list's entries
+ * inside r_c}: PE counts each half-list entry once and each full-list entry
+ * 1/2 (so row ranges partition the sum).  Overwrites out. */
+lj_status lj_energy(const double *q, const double *p, int64_t n, lj_geom g,
+                    int64_t row_begin, int64_t row_end,
+                    const int32_t *number_of_partners, const int64_t *pointer,
+                    const int32_t *sorted_list, int half, double *out, void *stream);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+
+const char *lj_status_string(lj_status s);
+const char *lj_last_error(void);
+/* Number of kernels this library has launched in the process (all threads). */
+long long lj_launch_count(void);
+/* Library version string. */
+const char *lj_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIBLJ_H */

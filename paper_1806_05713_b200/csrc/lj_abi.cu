@@ -1,0 +1,288 @@
+// extern "C" boundary of liblj.so (include/liblj.h): argument validation,
+// error mapping, workspace carving, launch bookkeeping.  No allocation here.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "lj_internal.cuh"
+
+namespace lj {
+std::atomic<long long> g_launches{0};
+}
+
+using namespace lj;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+lj_status fail(lj_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+lj_status fail(lj_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    t_last_error = buf;
+    return s;
+}
+
+lj_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return LJ_OK;
+    return fail(LJ_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
+
+lj_status check_geom(const lj_geom& g, bool need_box) {
+    if (!(g.rc > 0.0) || !(g.rs > g.rc) || !std::isfinite(g.rs))
+        return fail(LJ_ERR_ARG, "geometry: need 0 < rc < rs (rc=%g rs=%g)", g.rc, g.rs);
+    if (!(g.L >= 0.0) || !std::isfinite(g.L)) return fail(LJ_ERR_ARG, "geometry: L must be >= 0 (L=%g)", g.L);
+    if (g.L > 0.0 && std::floor(g.L / g.rs) < 3.0)
+        return fail(LJ_ERR_ARG, "geometry: floor(L/rs) must be >= 3 (L=%g rs=%g)", g.L, g.rs);
+    if (need_box && !(g.L > 0.0))
+        return fail(LJ_ERR_UNSUPPORTED, "list construction needs a periodic box (L > 0)");
+    return LJ_OK;
+}
+
+lj_status check_n(int64_t n) {
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(LJ_ERR_ARG, "n=%lld out of range [0, 2^31)", (long long)n);
+    return LJ_OK;
+}
+
+lj_status check_rows(int64_t n, int64_t b, int64_t e) {
+    if (b < 0 || b > e || e > n)
+        return fail(LJ_ERR_ARG, "row range [%lld,%lld) not within [0,%lld]", (long long)b, (long long)e, (long long)n);
+    return LJ_OK;
+}
+
+CellGrid make_grid(const lj_geom& g) {
+    CellGrid cg;
+    cg.L = g.L;
+    cg.nc = (int)std::floor(g.L / g.rs);
+    cg.inv_w = (double)cg.nc / g.L;
+    cg.ncell = (int64_t)cg.nc * cg.nc * cg.nc;
+    return cg;
+}
+
+#define LJ_TRY(x)                      \
+    do {                               \
+        lj_status _s = (x);            \
+        if (_s != LJ_OK) return _s;    \
+    } while (0)
+
+#define LJ_CUDA(x, where)                                 \
+    do {                                                  \
+        cudaError_t _e = (x);                             \
+        if (_e != cudaSuccess) return cuda_status(_e, where); \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char* lj_version(void) { return "liblj 0.1 (sm_100a, fp64)"; }
+
+long long lj_launch_count(void) { return g_launches.load(); }
+
+const char* lj_last_error(void) { return t_last_error.c_str(); }
+
+const char* lj_status_string(lj_status s) {
+    switch (s) {
+        case LJ_OK: return "LJ_OK";
+        case LJ_ERR_ARG: return "LJ_ERR_ARG";
+        case LJ_ERR_CAPACITY: return "LJ_ERR_CAPACITY";
+        case LJ_ERR_CUDA: return "LJ_ERR_CUDA";
+        case LJ_ERR_UNSUPPORTED: return "LJ_ERR_UNSUPPORTED";
+    }
+    return "LJ_UNKNOWN";
+}
+
+lj_status lj_pack_aos4(const double* xyz, double* out, int64_t n, void* stream) {
+    LJ_TRY(check_n(n));
+    if (n > 0 && (!xyz || !out)) return fail(LJ_ERR_ARG, "pack: null pointer");
+    if (!aligned32(out)) return fail(LJ_ERR_ARG, "pack: output not 32-byte aligned");
+    LJ_CUDA(launch_pack(xyz, out, n, (cudaStream_t)stream), "lj_pack_aos4");
+    return LJ_OK;
+}
+
+lj_status lj_unpack_aos4(const double* in, double* xyz, int64_t n, void* stream) {
+    LJ_TRY(check_n(n));
+    if (n > 0 && (!xyz || !in)) return fail(LJ_ERR_ARG, "unpack: null pointer");
+    if (!aligned32(in)) return fail(LJ_ERR_ARG, "unpack: input not 32-byte aligned");
+    LJ_CUDA(launch_unpack(in, xyz, n, (cudaStream_t)stream), "lj_unpack_aos4");
+    return LJ_OK;
+}
+
+lj_status lj_build_list_workspace(int64_t n, lj_geom g, size_t* bytes) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, true));
+    if (!bytes) return fail(LJ_ERR_ARG, "workspace: null output");
+    CellGrid cg = make_grid(g);
+    *bytes = build_workspace_layout(n, cg.ncell, n).total;
+    return LJ_OK;
+}
+
+lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
+                        int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list, int64_t capacity,
+                        int64_t* n_entries, void* workspace, size_t workspace_bytes, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, true));
+    LJ_TRY(check_rows(n, row_begin, row_end));
+    if (half && (row_begin != 0 || row_end != n))
+        return fail(LJ_ERR_UNSUPPORTED, "half list must cover all rows [0,n) (SURVEY §8(e))");
+    if (!n_entries || !pointer || (row_end > row_begin && !number_of_partners) || (n > 0 && !q))
+        return fail(LJ_ERR_ARG, "build_list: null pointer");
+    if (capacity < 0) return fail(LJ_ERR_ARG, "build_list: negative capacity");
+    if (capacity > 0 && !sorted_list) return fail(LJ_ERR_ARG, "build_list: null sorted_list with capacity > 0");
+    if (!aligned32(q)) return fail(LJ_ERR_ARG, "build_list: q not 32-byte aligned");
+    CellGrid cg = make_grid(g);
+    BuildWorkspace W = build_workspace_layout(n, cg.ncell, n);
+    if (!workspace || workspace_bytes < W.total)
+        return fail(LJ_ERR_ARG, "build_list: workspace too small (%zu < %zu)", workspace_bytes, W.total);
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+    const int64_t rows = row_end - row_begin;
+    const double rs2 = g.rs * g.rs;
+    LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
+    if (rows > 0)
+        LJ_CUDA(launch_list_count(q, n, cg, rs2, half, row_begin, row_end, number_of_partners, ws, W, s),
+                "lj_build_list/count");
+    LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, pointer, rows, (int64_t*)(ws + W.off_scan), W.scan_blocks, s),
+            "lj_build_list/scan");
+    int64_t total = 0;
+    LJ_CUDA(cudaMemcpyAsync(&total, pointer + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+            "lj_build_list/readback");
+    LJ_CUDA(cudaStreamSynchronize(s), "lj_build_list/sync");
+    *n_entries = total;
+    if (total > capacity)
+        return fail(LJ_ERR_CAPACITY, "build_list: capacity %lld < required %lld", (long long)capacity,
+                    (long long)total);
+    if (rows > 0 && total > 0)
+        LJ_CUDA(launch_list_fill(q, n, cg, rs2, half, row_begin, row_end, number_of_partners, pointer, sorted_list,
+                                 ws, W, s),
+                "lj_build_list/fill");
+    return LJ_OK;
+}
+
+lj_status lj_cell_order(const double* q, int64_t n, lj_geom g, int64_t* perm, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, true));
+    if (n > 0 && (!q || !perm)) return fail(LJ_ERR_ARG, "cell_order: null pointer");
+    if (!aligned32(q)) return fail(LJ_ERR_ARG, "cell_order: q not 32-byte aligned");
+    CellGrid cg = make_grid(g);
+    BuildWorkspace W = build_workspace_layout(n, cg.ncell, n);
+    if (!workspace || workspace_bytes < W.total)
+        return fail(LJ_ERR_ARG, "cell_order: workspace too small (%zu < %zu)", workspace_bytes, W.total);
+    cudaStream_t s = (cudaStream_t)stream;
+    LJ_CUDA(launch_cells(q, n, cg, (char*)workspace, W, s), "lj_cell_order/cells");
+    LJ_CUDA(launch_perm_from_cells(perm, n, (char*)workspace, W, s), "lj_cell_order/perm");
+    return LJ_OK;
+}
+
+lj_status lj_permute_rows(const double* in, double* out, const int64_t* perm, int64_t n, void* stream) {
+    LJ_TRY(check_n(n));
+    if (n > 0 && (!in || !out || !perm)) return fail(LJ_ERR_ARG, "permute: null pointer");
+    if (in == out && n > 0) return fail(LJ_ERR_ARG, "permute: in and out must differ");
+    if (!aligned32(in) || !aligned32(out)) return fail(LJ_ERR_ARG, "permute: records not 32-byte aligned");
+    LJ_CUDA(launch_permute(in, out, perm, n, (cudaStream_t)stream), "lj_permute_rows");
+    return LJ_OK;
+}
+
+lj_status lj_force_step_ex(const double* q, double* p, int64_t n, lj_geom g, double dt, int half, int64_t row_begin,
+                           int64_t row_end, const int32_t* number_of_partners, const int64_t* pointer,
+                           const int32_t* sorted_list, int lanes_per_row, int ordered,
+                           unsigned long long* n_interactions, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, false));
+    LJ_TRY(check_rows(n, row_begin, row_end));
+    if (!std::isfinite(dt)) return fail(LJ_ERR_ARG, "force: dt not finite");
+    if (half && (row_begin != 0 || row_end != n))
+        return fail(LJ_ERR_UNSUPPORTED, "half list must cover all rows [0,n) (its atomics write p of any atom)");
+    if (half && ordered) return fail(LJ_ERR_UNSUPPORTED, "ordered (bit-exact) mode exists for the full list only");
+    const int64_t rows = row_end - row_begin;
+    if (rows > 0 && (!q || !p || !number_of_partners || !pointer))
+        return fail(LJ_ERR_ARG, "force: null pointer");
+    if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "force: q/p not 32-byte aligned");
+    int lanes = lanes_per_row;
+    if (lanes == 0) lanes = half ? 8 : 8;
+    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
+        return fail(LJ_ERR_ARG, "force: lanes_per_row must be 0,1,2,4,8,16 or 32 (got %d)", lanes_per_row);
+    ForceArgs a;
+    a.q = q;
+    a.p = p;
+    a.row_begin = row_begin;
+    a.rows = rows;
+    a.npart = number_of_partners;
+    a.ptr = pointer;
+    a.list = sorted_list;
+    a.L = g.L;
+    a.rc2 = g.rc * g.rc;
+    a.dt = dt;
+    a.n_inter = n_interactions;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ordered)
+        LJ_CUDA(launch_force_ordered(a, s), "lj_force_step/ordered");
+    else if (half)
+        LJ_CUDA(launch_force_half(a, lanes, s), "lj_force_step/half");
+    else
+        LJ_CUDA(launch_force_full(a, lanes, s), "lj_force_step/full");
+    return LJ_OK;
+}
+
+lj_status lj_force_step(const double* q, double* p, int64_t n, lj_geom g, double dt, int half, int64_t row_begin,
+                        int64_t row_end, const int32_t* number_of_partners, const int64_t* pointer,
+                        const int32_t* sorted_list, void* stream) {
+    return lj_force_step_ex(q, p, n, g, dt, half, row_begin, row_end, number_of_partners, pointer, sorted_list, 0, 0,
+                            nullptr, stream);
+}
+
+lj_status lj_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, void* stream) {
+    if (begin < 0 || end < begin || end > (int64_t)INT32_MAX)
+        return fail(LJ_ERR_ARG, "integrate: bad range [%lld,%lld)", (long long)begin, (long long)end);
+    if (end > begin && (!q || !p)) return fail(LJ_ERR_ARG, "integrate: null pointer");
+    if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "integrate: q/p not 32-byte aligned");
+    if (!std::isfinite(dt)) return fail(LJ_ERR_ARG, "integrate: dt not finite");
+    LJ_CUDA(launch_integrate(q, p, begin, end, dt, (cudaStream_t)stream), "lj_integrate");
+    return LJ_OK;
+}
+
+lj_status lj_wrap(double* q, double* q_ref, int64_t n, double L, void* stream) {
+    LJ_TRY(check_n(n));
+    if (!(L > 0.0) || !std::isfinite(L)) return fail(LJ_ERR_ARG, "wrap: L must be > 0");
+    if (n > 0 && !q) return fail(LJ_ERR_ARG, "wrap: null q");
+    if (!aligned32(q) || !aligned32(q_ref)) return fail(LJ_ERR_ARG, "wrap: records not 32-byte aligned");
+    LJ_CUDA(launch_wrap(q, q_ref, n, L, (cudaStream_t)stream), "lj_wrap");
+    return LJ_OK;
+}
+
+lj_status lj_max_displacement(const double* q, const double* q_ref, int64_t begin, int64_t end, double* out,
+                              void* stream) {
+    if (begin < 0 || end < begin || end > (int64_t)INT32_MAX)
+        return fail(LJ_ERR_ARG, "max_displacement: bad range");
+    if (!out || (end > begin && (!q || !q_ref))) return fail(LJ_ERR_ARG, "max_displacement: null pointer");
+    if (!aligned32(q) || !aligned32(q_ref)) return fail(LJ_ERR_ARG, "max_displacement: not 32-byte aligned");
+    LJ_CUDA(launch_max_disp(q, q_ref, begin, end, out, (cudaStream_t)stream), "lj_max_displacement");
+    return LJ_OK;
+}
+
+lj_status lj_energy(const double* q, const double* p, int64_t n, lj_geom g, int64_t row_begin, int64_t row_end,
+                    const int32_t* number_of_partners, const int64_t* pointer, const int32_t* sorted_list, int half,
+                    double* out, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, false));
+    LJ_TRY(check_rows(n, row_begin, row_end));
+    if (!out) return fail(LJ_ERR_ARG, "energy: null out");
+    if (row_end > row_begin && (!q || !p || !number_of_partners || !pointer))
+        return fail(LJ_ERR_ARG, "energy: null pointer");
+    if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "energy: not 32-byte aligned");
+    LJ_CUDA(launch_energy(q, p, row_begin, row_end - row_begin, number_of_partners, pointer, sorted_list, g.L,
+                          g.rc * g.rc, g.rc, half, out, (cudaStream_t)stream),
+            "lj_energy");
+    return LJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,288 @@
+// LJ force step over the sorted (CSR) Verlet list -- SURVEY §8(a) a5/a6.
+//
+// The method (PAPER.md Alg. lj_force, inside Alg.
+// calcforce_sortedlist): for each i-atom, for each j in
+// SortedList[i]: r = q_j - q_i; if r^2 < r_c^2: df = (48 - 24 r^6) dt / r^14,
+// p_i -= df r (and p_j += df r for the half list; Newton-3 sign, reading C-1).
+//
+// B200 mapping (the paper's SIMD tricks are prior art):
+//  * "i-data in registers": G lanes cooperate on one row; q_i and
+//    the three accumulators stay in registers; the G partial sums are reduced
+//    with warp shuffles and p_i is committed once (no atomics, full list).
+//  * "AoS with padding": every partner gather is ONE 256-bit load
+//    (LDG.E.ENL2.256) of a 32-byte record = one L2 sector.
+//  * cutoff masking and remainder-loop elimination:
+//    out-of-range pairs get df = 0 by a predicate (integer compare of the
+//    IEEE bits of r^2 and r_c^2, exact for positive doubles); tail lanes
+//    k >= n_i are simply inactive in the last group iteration.
+//  * software pipelining: two independent partner gathers are in
+//    flight per lane (memory-level parallelism instead of IPC tricks).
+//  * fp64 division: 1/r^2 by MUFU.RCP64H (rcp.approx.ftz.f64) + one cubic
+//    Newton correction y(1 + e + e^2), e = 1 - r^2 y, then the 1/r^2 form
+//    df = dt (48 r^-6 - 24) r^-6 r^-2, algebraically the paper's expression.
+//  * minimum image: raw differences are checked with integer ops on the high
+//    words; the three image DADDs run only when some lane of the warp needs an
+//    image (warp-uniform branch), i.e. only for rows near a box face.
+#include <climits>
+
+#include "lj_internal.cuh"
+
+namespace lj {
+
+namespace {
+
+constexpr int kForceThreads = 256;
+
+struct PairConsts {
+    double L;        // box side (0 = open)
+    double c48, c24; // 48 dt, 24 dt
+    long long rc2_bits;
+    int hi_halfL;    // high word of L/2 (INT_MAX for open boundaries)
+};
+
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    return fma(y, fma(e, e, e), y);
+}
+
+// |d| > L/2 (up to the low word; pairs that close to L/2 are never neighbours)
+__device__ __forceinline__ bool beyond_half(double d, int hi_halfL) {
+    return (__double2hiint(d) & 0x7fffffff) > hi_halfL;
+}
+
+__device__ __forceinline__ double image_shift(double d, double L, int hi_halfL) {
+    int hi = __double2hiint(d);
+    double s = ((hi & 0x7fffffff) > hi_halfL) ? L : 0.0;
+    return hi < 0 ? -s : s;
+}
+
+// One list entry: returns the impulse coefficient df (0 if r >= r_c) and the
+// minimum-image relative vector in dx, dy, dz.
+__device__ __forceinline__ double pair_df(const rec4& qi, const rec4& qj, const PairConsts& c, double& dx, double& dy,
+                                          double& dz, bool& inside) {
+    dx = qj.x - qi.x;
+    dy = qj.y - qi.y;
+    dz = qj.z - qi.z;
+    bool need = beyond_half(dx, c.hi_halfL) | beyond_half(dy, c.hi_halfL) | beyond_half(dz, c.hi_halfL);
+    if (__any_sync(__activemask(), need)) {
+        dx -= image_shift(dx, c.L, c.hi_halfL);
+        dy -= image_shift(dy, c.L, c.hi_halfL);
+        dz -= image_shift(dz, c.L, c.hi_halfL);
+    }
+    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double inv2 = fast_rcp(r2);
+    double inv6 = inv2 * inv2 * inv2;
+    double df = fma(c.c48, inv6, -c.c24) * (inv6 * inv2);
+    inside = __double_as_longlong(r2) < c.rc2_bits;
+    return inside ? df : 0.0;
+}
+
+template <int G>
+__device__ __forceinline__ void group_reduce(double& ax, double& ay, double& az, unsigned& cnt) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        ax += __shfl_xor_sync(0xffffffffu, ax, o);
+        ay += __shfl_xor_sync(0xffffffffu, ay, o);
+        az += __shfl_xor_sync(0xffffffffu, az, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+}
+
+__device__ __forceinline__ void count_interactions(unsigned cnt, unsigned long long* n_inter) {
+    if (n_inter == nullptr) return;
+    unsigned long long v = cnt;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(n_inter, v);
+}
+
+// Full list: G lanes per row, no atomics, p_i committed once by lane 0 of the group.
+template <int G, bool HALF>
+__global__ void __launch_bounds__(kForceThreads)
+    k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
+            const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
+            PairConsts c, unsigned long long* n_inter) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    const bool active = r < rows;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    unsigned cnt = 0;
+    if (active) {
+        const int64_t i = row_begin + r;
+        const rec4 qi = load_rec(q, i);
+        const int32_t* __restrict__ lst = list + ptr[r];
+        const int n = npart[r];
+        int k = g;
+        for (; k + G < n; k += 2 * G) {
+            const int j0 = __ldg(lst + k), j1 = __ldg(lst + k + G);
+            const rec4 q0 = load_rec(q, j0), q1 = load_rec(q, j1);
+            double dx0, dy0, dz0, dx1, dy1, dz1;
+            bool in0, in1;
+            double df0 = pair_df(qi, q0, c, dx0, dy0, dz0, in0);
+            double df1 = pair_df(qi, q1, c, dx1, dy1, dz1, in1);
+            ax = fma(-df0, dx0, ax);
+            ay = fma(-df0, dy0, ay);
+            az = fma(-df0, dz0, az);
+            ax = fma(-df1, dx1, ax);
+            ay = fma(-df1, dy1, ay);
+            az = fma(-df1, dz1, az);
+            cnt += in0 + in1;
+            if (HALF) {
+                if (in0) {
+                    atomicAdd(&p[j0].x, df0 * dx0);
+                    atomicAdd(&p[j0].y, df0 * dy0);
+                    atomicAdd(&p[j0].z, df0 * dz0);
+                }
+                if (in1) {
+                    atomicAdd(&p[j1].x, df1 * dx1);
+                    atomicAdd(&p[j1].y, df1 * dy1);
+                    atomicAdd(&p[j1].z, df1 * dz1);
+                }
+            }
+        }
+        if (k < n) {
+            const int j0 = __ldg(lst + k);
+            const rec4 q0 = load_rec(q, j0);
+            double dx0, dy0, dz0;
+            bool in0;
+            double df0 = pair_df(qi, q0, c, dx0, dy0, dz0, in0);
+            ax = fma(-df0, dx0, ax);
+            ay = fma(-df0, dy0, ay);
+            az = fma(-df0, dz0, az);
+            cnt += in0;
+            if (HALF && in0) {
+                atomicAdd(&p[j0].x, df0 * dx0);
+                atomicAdd(&p[j0].y, df0 * dy0);
+                atomicAdd(&p[j0].z, df0 * dz0);
+            }
+        }
+    }
+    unsigned cnt_row = cnt;
+    group_reduce<G>(ax, ay, az, cnt_row);
+    if (active && g == 0) {
+        const int64_t i = row_begin + r;
+        if (HALF) {
+            // p_i is concurrently a RED target of earlier rows (i in row(i'), i' < i):
+            // commit with REDs too (SURVEY §8(a) a6 race hazard).
+            atomicAdd(&p[i].x, ax);
+            atomicAdd(&p[i].y, ay);
+            atomicAdd(&p[i].z, az);
+        } else {
+            rec4 pi = p[i];
+            pi.x += ax;
+            pi.y += ay;
+            pi.z += az;
+            p[i] = pi;   // pad preserved (read back unchanged)
+        }
+    }
+    count_interactions(cnt, n_inter);
+}
+
+// Bit-exact "ordered" full-list kernel (DESIGN.md Pin-11): one thread per row,
+// ascending j, Alg. 3 accumulating into the loaded p_i, the oracle's expression
+// order and IEEE operations (explicit _rn intrinsics: no FMA contraction).
+__device__ __forceinline__ double min_image_exact(double d, double L) {
+    if (L > 0.0) {
+        if (d > 0.5 * L)
+            d = __dsub_rn(d, L);
+        else if (d < -0.5 * L)
+            d = __dadd_rn(d, L);
+    }
+    return d;
+}
+
+__global__ void __launch_bounds__(kForceThreads)
+    k_force_ordered(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
+                    const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr,
+                    const int32_t* __restrict__ list, double L, double rc2, double dt, unsigned long long* n_inter) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned cnt = 0;
+    if (r < rows) {
+        const int64_t i = row_begin + r;
+        const rec4 qi = load_rec(q, i);
+        rec4 pi = p[i];
+        const int64_t beg = ptr[r];
+        const int n = npart[r];
+        for (int k = 0; k < n; k++) {
+            const rec4 qj = load_rec(q, list[beg + k]);
+            double dx = min_image_exact(__dsub_rn(qj.x, qi.x), L);
+            double dy = min_image_exact(__dsub_rn(qj.y, qi.y), L);
+            double dz = min_image_exact(__dsub_rn(qj.z, qi.z), L);
+            double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            if (r2 < rc2) {
+                double r6 = __dmul_rn(__dmul_rn(r2, r2), r2);
+                double r14 = __dmul_rn(__dmul_rn(r6, r6), r2);
+                double df = __ddiv_rn(__dmul_rn(__dsub_rn(48.0, __dmul_rn(24.0, r6)), dt), r14);
+                pi.x = __dsub_rn(pi.x, __dmul_rn(df, dx));
+                pi.y = __dsub_rn(pi.y, __dmul_rn(df, dy));
+                pi.z = __dsub_rn(pi.z, __dmul_rn(df, dz));
+                cnt++;
+            }
+        }
+        p[i] = pi;
+    }
+    count_interactions(cnt, n_inter);
+}
+
+PairConsts make_consts(const ForceArgs& a) {
+    PairConsts c;
+    c.L = a.L;
+    c.c48 = 48.0 * a.dt;
+    c.c24 = 24.0 * a.dt;
+    union {
+        double d;
+        long long b;
+    } u;
+    u.d = a.rc2;
+    c.rc2_bits = u.b;
+    if (a.L > 0.0) {
+        u.d = 0.5 * a.L;
+        c.hi_halfL = (int)(u.b >> 32);
+    } else {
+        c.hi_halfL = INT_MAX;
+    }
+    return c;
+}
+
+template <bool HALF>
+cudaError_t launch_g(const ForceArgs& a, int lanes, cudaStream_t s) {
+    if (a.rows <= 0) return cudaSuccess;
+    PairConsts c = make_consts(a);
+    int64_t threads = a.rows * (int64_t)lanes;
+    unsigned grid = (unsigned)((threads + kForceThreads - 1) / kForceThreads);
+    const rec4* q = (const rec4*)a.q;
+    rec4* p = (rec4*)a.p;
+#define LJ_LAUNCH(G)                                                                                        \
+    k_force<G, HALF><<<grid, kForceThreads, 0, s>>>(q, p, a.row_begin, a.rows, a.npart, a.ptr, a.list, c, \
+                                                     a.n_inter)
+    switch (lanes) {
+        case 1: LJ_LAUNCH(1); break;
+        case 2: LJ_LAUNCH(2); break;
+        case 4: LJ_LAUNCH(4); break;
+        case 8: LJ_LAUNCH(8); break;
+        case 16: LJ_LAUNCH(16); break;
+        case 32: LJ_LAUNCH(32); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef LJ_LAUNCH
+    g_launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_force_full(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_g<false>(a, lanes, s); }
+cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_g<true>(a, lanes, s); }
+
+cudaError_t launch_force_ordered(const ForceArgs& a, cudaStream_t s) {
+    if (a.rows <= 0) return cudaSuccess;
+    unsigned grid = (unsigned)((a.rows + kForceThreads - 1) / kForceThreads);
+    k_force_ordered<<<grid, kForceThreads, 0, s>>>((const rec4*)a.q, (rec4*)a.p, a.row_begin, a.rows, a.npart, a.ptr,
+                                                   a.list, a.L, a.rc2, a.dt, a.n_inter);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace lj

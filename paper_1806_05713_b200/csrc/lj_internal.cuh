@@ -1,0 +1,93 @@
+// Internal declarations shared by the liblj CUDA translation units.
+// (Product code only -- nothing here is shared with oracle/.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "../../include/liblj.h"
+
+namespace lj {
+
+// The paper's "AoS with padding" record: x, y, z, pad.
+// 32-byte alignment makes one record exactly one 256-bit load (LDG.E.ENL2.256
+// on sm_100a) and exactly one 32-byte L2 sector.
+struct __align__(32) rec4 {
+    double x, y, z, w;
+};
+
+extern std::atomic<long long> g_launches;
+
+// 256-bit read-only load of one record (compiles to LDG.E.ENL2.256.CONSTANT).
+__device__ __forceinline__ rec4 load_rec(const rec4* __restrict__ a, int64_t i) {
+    rec4 r;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+                 : "l"(a + i));
+    return r;
+}
+
+// Cell geometry shared by the list builder and the cell-order pass.
+struct CellGrid {
+    double L, inv_w;   // inv_w = nc / L
+    int nc;
+    int64_t ncell;
+};
+
+// Workspace carve-out (offsets in bytes, 256-B aligned).
+struct BuildWorkspace {
+    size_t off_cell_of, off_count, off_start, off_cursor, off_atoms, off_qcell, off_scan, off_misc, total;
+    int64_t scan_blocks;
+};
+
+BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows);
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* ws, const BuildWorkspace& W,
+                         cudaStream_t s);
+cudaError_t launch_list_count(const double* q, int64_t n, const CellGrid& cg, double rs2, int half,
+                              int64_t row_begin, int64_t row_end, int32_t* npart, char* ws,
+                              const BuildWorkspace& W, cudaStream_t s);
+cudaError_t launch_list_fill(const double* q, int64_t n, const CellGrid& cg, double rs2, int half,
+                             int64_t row_begin, int64_t row_end, const int32_t* npart, const int64_t* ptr,
+                             int32_t* list, char* ws, const BuildWorkspace& W, cudaStream_t s);
+// exclusive scan of int32 counts -> int64 offsets (out has n+1 entries)
+cudaError_t launch_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, int64_t* block_sums,
+                                   int64_t nblocks, cudaStream_t s);
+cudaError_t launch_perm_from_cells(int64_t* perm, int64_t n, char* ws, const BuildWorkspace& W, cudaStream_t s);
+cudaError_t launch_permute(const double* in, double* out, const int64_t* perm, int64_t n, cudaStream_t s);
+
+struct ForceArgs {
+    const double* q;
+    double* p;
+    int64_t row_begin, rows;
+    const int32_t* npart;
+    const int64_t* ptr;
+    const int32_t* list;
+    double L, rc2, dt;
+    unsigned long long* n_inter;
+};
+cudaError_t launch_force_full(const ForceArgs& a, int lanes, cudaStream_t s);
+cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s);
+cudaError_t launch_force_ordered(const ForceArgs& a, cudaStream_t s);
+
+cudaError_t launch_pack(const double* xyz, double* out, int64_t n, cudaStream_t s);
+cudaError_t launch_unpack(const double* in, double* xyz, int64_t n, cudaStream_t s);
+cudaError_t launch_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, cudaStream_t s);
+cudaError_t launch_wrap(double* q, double* q_ref, int64_t n, double L, cudaStream_t s);
+cudaError_t launch_max_disp(const double* q, const double* q_ref, int64_t begin, int64_t end, double* out,
+                            cudaStream_t s);
+cudaError_t launch_energy(const double* q, const double* p, int64_t row_begin, int64_t rows, const int32_t* npart,
+                          const int64_t* ptr, const int32_t* list, double L, double rc2, double rc, int half,
+                          double* out, cudaStream_t s);
+
+inline int grid_for(int64_t work, int block, int max_blocks = 148 * 64) {
+    int64_t g = (work + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (int)g;
+}
+
+}  // namespace lj

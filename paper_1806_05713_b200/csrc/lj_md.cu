@@ -1,0 +1,196 @@
+// Streaming kernels around the force step:
+// AoS4 pack/unpack, drift, wrap + bookkeeping snapshot, max displacement, energy.
+// All are HBM-streaming (one pass over 32-B records); integrate, wrap and the
+// displacement are bit-identical to the oracle (explicit _rn intrinsics).
+#include "lj_internal.cuh"
+
+namespace lj {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void k_pack(const double* __restrict__ xyz, rec4* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        rec4 r;
+        r.x = xyz[3 * i];
+        r.y = xyz[3 * i + 1];
+        r.z = xyz[3 * i + 2];
+        r.w = 0.0;
+        out[i] = r;
+    }
+}
+
+__global__ void k_unpack(const rec4* __restrict__ in, double* __restrict__ xyz, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        rec4 r = in[i];
+        xyz[3 * i] = r.x;
+        xyz[3 * i + 1] = r.y;
+        xyz[3 * i + 2] = r.z;
+    }
+}
+
+// q_i += p_i dt (mass 1), same rounding as the oracle: q + (p*dt), no FMA.
+__global__ void k_integrate(rec4* __restrict__ q, const rec4* __restrict__ p, int64_t begin, int64_t end,
+                            double dt) {
+    for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        rec4 a = q[i];
+        const rec4 b = p[i];
+        a.x = __dadd_rn(a.x, __dmul_rn(b.x, dt));
+        a.y = __dadd_rn(a.y, __dmul_rn(b.y, dt));
+        a.z = __dadd_rn(a.z, __dmul_rn(b.z, dt));
+        q[i] = a;
+    }
+}
+
+__device__ __forceinline__ double wrap1(double x, double L) {
+    double w = __dsub_rn(x, __dmul_rn(L, floor(__ddiv_rn(x, L))));
+    if (w >= L) w = __dsub_rn(w, L);
+    return w;
+}
+
+__global__ void k_wrap(rec4* __restrict__ q, rec4* __restrict__ q_ref, int64_t n, double L) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        rec4 a = q[i];
+        a.x = wrap1(a.x, L);
+        a.y = wrap1(a.y, L);
+        a.z = wrap1(a.z, L);
+        q[i] = a;
+        if (q_ref) q_ref[i] = a;
+    }
+}
+
+__device__ __forceinline__ double block_max(double v) {
+    __shared__ double s[32];
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) s[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? s[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+    return v;
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double s[32];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) s[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? s[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+
+// max_i |q_i - q_ref_i| (Euclidean, sqrt((dx*dx + dy*dy) + dz*dz) as the oracle).
+// Non-negative doubles order like their bit patterns -> atomicMax on uint64.
+__global__ void k_max_disp(const rec4* __restrict__ q, const rec4* __restrict__ q_ref, int64_t begin, int64_t end,
+                           unsigned long long* out) {
+    double m = 0.0;
+    for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const rec4 a = q[i], b = q_ref[i];
+        double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y), dz = __dsub_rn(a.z, b.z);
+        double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        m = fmax(m, d);
+    }
+    m = block_max(m);
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// KE over own rows and shifted PE over list entries inside r_c (thread per row).
+__global__ void k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p, int64_t row_begin, int64_t rows,
+                         const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr,
+                         const int32_t* __restrict__ list, double L, double rc2, double vc, int half,
+                         double* out) {
+    double ke = 0.0, pe = 0.0;
+    const double halfL = 0.5 * L;
+    const double w = half ? 1.0 : 0.5;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = row_begin + r;
+        const rec4 qi = q[i], pi = p[i];
+        ke += 0.5 * (pi.x * pi.x + pi.y * pi.y + pi.z * pi.z);
+        const int64_t beg = ptr[r];
+        const int n = npart[r];
+        for (int k = 0; k < n; k++) {
+            const rec4 qj = load_rec(q, list[beg + k]);
+            double d[3] = {qj.x - qi.x, qj.y - qi.y, qj.z - qi.z};
+            if (L > 0.0) {
+#pragma unroll
+                for (int c = 0; c < 3; c++) d[c] = d[c] > halfL ? d[c] - L : (d[c] < -halfL ? d[c] + L : d[c]);
+            }
+            double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+            if (r2 < rc2) {
+                double inv6 = 1.0 / (r2 * r2 * r2);
+                pe += w * (4.0 * (inv6 * inv6 - inv6) - vc);
+            }
+        }
+    }
+    ke = block_sum(ke);
+    pe = block_sum(pe);
+    if (threadIdx.x == 0) {
+        atomicAdd(&out[0], ke);
+        atomicAdd(&out[1], pe);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_pack(const double* xyz, double* out, int64_t n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_pack<<<grid_for(n, kThreads), kThreads, 0, s>>>(xyz, (rec4*)out, n);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const double* in, double* xyz, int64_t n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_unpack<<<grid_for(n, kThreads), kThreads, 0, s>>>((const rec4*)in, xyz, n);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, cudaStream_t s) {
+    if (end <= begin) return cudaSuccess;
+    k_integrate<<<grid_for(end - begin, kThreads), kThreads, 0, s>>>((rec4*)q, (const rec4*)p, begin, end, dt);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wrap(double* q, double* q_ref, int64_t n, double L, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_wrap<<<grid_for(n, kThreads), kThreads, 0, s>>>((rec4*)q, (rec4*)q_ref, n, L);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_max_disp(const double* q, const double* q_ref, int64_t begin, int64_t end, double* out,
+                            cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+    if (e != cudaSuccess || end <= begin) return e;
+    k_max_disp<<<grid_for(end - begin, kThreads, 148 * 8), kThreads, 0, s>>>(
+        (const rec4*)q, (const rec4*)q_ref, begin, end, (unsigned long long*)out);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energy(const double* q, const double* p, int64_t row_begin, int64_t rows, const int32_t* npart,
+                          const int64_t* ptr, const int32_t* list, double L, double rc2, double rc, int half,
+                          double* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), s);
+    if (e != cudaSuccess || rows <= 0) return e;
+    double rc6 = rc2 * rc2 * rc2;
+    double vc = 4.0 * (1.0 / (rc6 * rc6) - 1.0 / rc6);
+    k_energy<<<grid_for(rows, kThreads, 148 * 8), kThreads, 0, s>>>((const rec4*)q, (const rec4*)p, row_begin, rows,
+                                                                   npart, ptr, list, L, rc2, vc, half, out);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace lj

@@ -1,0 +1,274 @@
+"""Thin Python binding of liblj.so (include/liblj.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module
+checks tensor dtype/device/shape/contiguity, passes raw device pointers and
+torch's current CUDA stream, and raises LJError on a non-OK status.  There is
+no CPU fallback: if liblj.so is missing or no GPU is present, calls fail.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblj.so")
+
+LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+
+# every symbol include/liblj.h declares
+EXPORTS = (
+    "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_cell_order",
+    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_integrate", "lj_wrap",
+    "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
+    "lj_version",
+)
+
+
+class LJError(RuntimeError):
+    def __init__(self, status, detail):
+        super().__init__(f"{_STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+_STATUS = {0: "LJ_OK", 1: "LJ_ERR_ARG", 2: "LJ_ERR_CAPACITY", 3: "LJ_ERR_CUDA", 4: "LJ_ERR_UNSUPPORTED"}
+
+
+class Geom(ctypes.Structure):
+    """lj_geom: L (0 = open), rc (cutoff), rs (search length)."""
+    _fields_ = [("L", ctypes.c_double), ("rc", ctypes.c_double), ("rs", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load liblj.so (built in-tree by paper_1806_05713_b200/build.py).  Fails loudly."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"liblj.so not built ({LIB_PATH}); run python -c 'import __graft_entry__ as g; g.build()'")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, d, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+    st = ctypes.c_int
+    sig = {
+        "lj_pack_aos4": (st, [vp, vp, i64, vp]),
+        "lj_unpack_aos4": (st, [vp, vp, i64, vp]),
+        "lj_build_list_workspace": (st, [i64, Geom, ctypes.POINTER(sz)]),
+        "lj_build_list": (st, [vp, i64, Geom, i32, i64, i64, vp, vp, vp, i64, ctypes.POINTER(i64), vp, sz, vp]),
+        "lj_cell_order": (st, [vp, i64, Geom, vp, vp, sz, vp]),
+        "lj_permute_rows": (st, [vp, vp, vp, i64, vp]),
+        "lj_force_step": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, vp]),
+        "lj_force_step_ex": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, i32, i32, vp, vp]),
+        "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
+        "lj_wrap": (st, [vp, vp, i64, d, vp]),
+        "lj_max_displacement": (st, [vp, vp, i64, i64, vp, vp]),
+        "lj_energy": (st, [vp, vp, i64, Geom, i64, i64, vp, vp, vp, i32, vp, vp]),
+        "lj_status_string": (ctypes.c_char_p, [st]),
+        "lj_last_error": (ctypes.c_char_p, []),
+        "lj_launch_count": (ctypes.c_longlong, []),
+        "lj_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status):
+    if status != LJ_OK:
+        raise LJError(status, load().lj_last_error().decode())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _rec(t, name):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.dim() == 2
+            and t.shape[1] == 4 and t.is_contiguous()):
+        raise TypeError(f"{name}: need a contiguous CUDA float64 (n,4) tensor (AoS4 records)")
+    return t
+
+
+def geom(L, rc, rs) -> Geom:
+    return Geom(float(L), float(rc), float(rs))
+
+
+def launch_count() -> int:
+    return int(load().lj_launch_count())
+
+
+def version() -> str:
+    return load().lj_version().decode()
+
+
+# ---- layout ---------------------------------------------------------------
+
+def pack_aos4(xyz: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(n,3) float64 CUDA -> (n,4) AoS4 records, pad 0."""
+    if not (xyz.is_cuda and xyz.dtype == torch.float64 and xyz.dim() == 2 and xyz.shape[1] == 3):
+        raise TypeError("pack_aos4: need a CUDA float64 (n,3) tensor")
+    xyz = xyz.contiguous()
+    n = xyz.shape[0]
+    if out is None:
+        out = torch.empty((n, 4), dtype=torch.float64, device=xyz.device)
+    _check(load().lj_pack_aos4(_ptr(xyz), _ptr(_rec(out, "out")), n, _stream()))
+    return out
+
+
+def unpack_aos4(q: torch.Tensor) -> torch.Tensor:
+    _rec(q, "q")
+    out = torch.empty((q.shape[0], 3), dtype=torch.float64, device=q.device)
+    _check(load().lj_unpack_aos4(_ptr(q), _ptr(out), q.shape[0], _stream()))
+    return out
+
+
+# ---- lists ------------------------------------------------------------------
+
+@dataclasses.dataclass
+class CSRList:
+    """Row-local sorted list (PAPER.md Fig. sorted_list) on the device."""
+    number_of_partners: torch.Tensor   # int32 [rows]
+    pointer: torch.Tensor              # int64 [rows+1]
+    sorted_list: torch.Tensor          # int32 [capacity] (first n_entries valid)
+    n_entries: int
+    row_begin: int
+    row_end: int
+    half: bool
+
+    @property
+    def rows(self):
+        return self.row_end - self.row_begin
+
+
+class ListBuilder:
+    """Holds the build workspace and a growing list buffer for repeated rebuilds."""
+
+    def __init__(self, n: int, g: Geom, half: bool, row_begin: int = 0, row_end: int | None = None,
+                 device=None, headroom: float = 1.15, initial_per_row: int = 0):
+        self.n, self.g, self.half = int(n), g, bool(half)
+        self.row_begin = int(row_begin)
+        self.row_end = int(n if row_end is None else row_end)
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self.headroom = headroom
+        b = ctypes.c_size_t(0)
+        _check(load().lj_build_list_workspace(self.n, g, ctypes.byref(b)))
+        self.workspace = torch.empty(max(int(b.value), 1), dtype=torch.uint8, device=self.device)
+        rows = self.row_end - self.row_begin
+        self.npart = torch.empty(max(rows, 1), dtype=torch.int32, device=self.device)
+        self.pointer = torch.empty(rows + 1, dtype=torch.int64, device=self.device)
+        self.sorted_list = torch.empty(max(int(rows * initial_per_row), 1), dtype=torch.int32, device=self.device)
+        self.rebuilds = 0
+
+    def build(self, q: torch.Tensor) -> CSRList:
+        _rec(q, "q")
+        L = load()
+        ne = ctypes.c_int64(0)
+        for _ in range(2):
+            st = L.lj_build_list(_ptr(q), self.n, self.g, int(self.half), self.row_begin, self.row_end,
+                                 _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
+                                 self.sorted_list.numel(), ctypes.byref(ne), _ptr(self.workspace),
+                                 self.workspace.numel(), _stream())
+            if st == LJ_ERR_CAPACITY:
+                cap = int(ne.value * self.headroom) + 1024
+                self.sorted_list = torch.empty(cap, dtype=torch.int32, device=self.device)
+                continue
+            _check(st)
+            break
+        else:
+            raise LJError(LJ_ERR_CAPACITY, "list capacity did not converge")
+        self.rebuilds += 1
+        rows = self.row_end - self.row_begin
+        return CSRList(self.npart[:rows], self.pointer, self.sorted_list, int(ne.value), self.row_begin,
+                       self.row_end, self.half)
+
+
+def build_list(q: torch.Tensor, g: Geom, half: bool, row_begin: int = 0, row_end: int | None = None) -> CSRList:
+    """One-shot lj_build_list (allocates its own workspace and exact-size list)."""
+    b = ListBuilder(q.shape[0], g, half, row_begin, row_end, device=q.device, headroom=1.0)
+    return b.build(q)
+
+
+def cell_order(q: torch.Tensor, g: Geom) -> torch.Tensor:
+    """perm[new] = old: stable sort by cell id (BASELINE.json config 3)."""
+    _rec(q, "q")
+    n = q.shape[0]
+    b = ctypes.c_size_t(0)
+    _check(load().lj_build_list_workspace(n, g, ctypes.byref(b)))
+    ws = torch.empty(max(int(b.value), 1), dtype=torch.uint8, device=q.device)
+    perm = torch.empty(n, dtype=torch.int64, device=q.device)
+    _check(load().lj_cell_order(_ptr(q), n, g, _ptr(perm), _ptr(ws), ws.numel(), _stream()))
+    return perm
+
+
+def permute_rows(x: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
+    _rec(x, "x")
+    if not (perm.is_cuda and perm.dtype == torch.int64 and perm.numel() == x.shape[0]):
+        raise TypeError("permute_rows: perm must be a CUDA int64 tensor of length n")
+    out = torch.empty_like(x)
+    _check(load().lj_permute_rows(_ptr(x), _ptr(out), _ptr(perm.contiguous()), x.shape[0], _stream()))
+    return out
+
+
+# ---- force / integrate / bookkeeping / energy ---------------------------------
+
+def _list_args(lst: CSRList):
+    return (lst.row_begin, lst.row_end, _ptr(lst.number_of_partners), _ptr(lst.pointer), _ptr(lst.sorted_list))
+
+
+def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRList, lanes_per_row: int = 0,
+               ordered: bool = False, n_interactions: torch.Tensor | None = None) -> None:
+    """p += impulses of one force step (in place).  PAPER.md Alg. 1 + Alg. 3."""
+    _rec(q, "q")
+    _rec(p, "p")
+    if n_interactions is not None and not (n_interactions.is_cuda and n_interactions.dtype == torch.int64):
+        raise TypeError("n_interactions must be a CUDA int64 tensor")
+    _check(load().lj_force_step_ex(_ptr(q), _ptr(p), q.shape[0], g, float(dt), int(lst.half), *_list_args(lst),
+                                   int(lanes_per_row), int(ordered), _ptr(n_interactions), _stream()))
+
+
+def integrate(q: torch.Tensor, p: torch.Tensor, dt: float, begin: int = 0, end: int | None = None) -> None:
+    _rec(q, "q")
+    _rec(p, "p")
+    _check(load().lj_integrate(_ptr(q), _ptr(p), int(begin), q.shape[0] if end is None else int(end), float(dt),
+                               _stream()))
+
+
+def wrap(q: torch.Tensor, L: float, q_ref: torch.Tensor | None = None) -> None:
+    _rec(q, "q")
+    if q_ref is not None:
+        _rec(q_ref, "q_ref")
+    _check(load().lj_wrap(_ptr(q), _ptr(q_ref), q.shape[0], float(L), _stream()))
+
+
+def max_displacement(q: torch.Tensor, q_ref: torch.Tensor, begin: int = 0, end: int | None = None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    _rec(q, "q")
+    _rec(q_ref, "q_ref")
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=q.device)
+    _check(load().lj_max_displacement(_ptr(q), _ptr(q_ref), int(begin), q.shape[0] if end is None else int(end),
+                                      _ptr(out), _stream()))
+    return out
+
+
+def energy(q: torch.Tensor, p: torch.Tensor, g: Geom, lst: CSRList, out: torch.Tensor | None = None) -> torch.Tensor:
+    """{KE over own rows, PE over the list's entries inside r_c} as a device (2,) tensor."""
+    _rec(q, "q")
+    _rec(p, "p")
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=q.device)
+    rb, re_, npp, ptr, sl = _list_args(lst)
+    _check(load().lj_energy(_ptr(q), _ptr(p), q.shape[0], g, rb, re_, npp, ptr, sl, int(lst.half), _ptr(out),
+                            _stream()))
+    return out

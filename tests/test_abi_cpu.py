@@ -1,0 +1,90 @@
+"""CPU-side checks of the C-ABI library (no GPU): it loads, exports every symbol
+include/liblj.h declares, and rejects bad arguments before launching anything."""
+import ctypes
+import re
+import os
+
+import pytest
+
+from paper_1806_05713_b200 import build, lj
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    build.build()
+    return lj.load()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "liblj.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lj_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_binding_exports():
+    assert declared_symbols() == sorted(lj.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(L):
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    out = os.popen(f"nm -D --defined-only {lj.LIB_PATH}").read()
+    for name in declared_symbols():
+        assert re.search(rf"\bT {name}\b", out), f"{name} not exported as a text symbol"
+
+
+def test_library_is_sm100a(L):
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {lj.LIB_PATH}").read()
+    assert "sm_100a" in out
+
+
+def test_version_and_counters(L):
+    assert b"sm_100a" in L.lj_version()
+    assert L.lj_launch_count() >= 0
+    assert L.lj_status_string(2) == b"LJ_ERR_CAPACITY"
+
+
+def test_validation_before_launch(L):
+    g_bad = lj.Geom(10.0, 3.3, 3.0)          # rc > rs
+    size = ctypes.c_size_t()
+    assert L.lj_build_list_workspace(100, g_bad, ctypes.byref(size)) == lj.LJ_ERR_ARG
+    assert b"rc" in L.lj_last_error()
+    g_small = lj.Geom(9.0, 3.0, 3.3)         # floor(9/3.3) = 2 < 3 cells
+    assert L.lj_build_list_workspace(100, g_small, ctypes.byref(size)) == lj.LJ_ERR_ARG
+    g_open = lj.Geom(0.0, 3.0, 3.3)          # list build needs a box
+    assert L.lj_build_list_workspace(100, g_open, ctypes.byref(size)) == lj.LJ_ERR_UNSUPPORTED
+    g = lj.Geom(15.874011, 3.0, 3.3)
+    assert L.lj_build_list_workspace(4000, g, ctypes.byref(size)) == lj.LJ_OK and size.value > 4000 * 40
+    assert L.lj_build_list_workspace(-1, g, ctypes.byref(size)) == lj.LJ_ERR_ARG
+    assert L.lj_build_list_workspace(2 ** 31, g, ctypes.byref(size)) == lj.LJ_ERR_ARG
+    # half list with a partial row range
+    ne = ctypes.c_int64()
+    st = L.lj_build_list(ctypes.c_void_p(256), 4000, g, 1, 0, 10, ctypes.c_void_p(256), ctypes.c_void_p(256), None, 0,
+                         ctypes.byref(ne), ctypes.c_void_p(256), 1 << 30, None)
+    assert st == lj.LJ_ERR_UNSUPPORTED
+    # bad row range / misaligned records / non-finite dt
+    st = L.lj_force_step(ctypes.c_void_p(256), ctypes.c_void_p(256), 10, g, 0.01, 0, 5, 3, None, None, None, None)
+    assert st == lj.LJ_ERR_ARG
+    st = L.lj_integrate(ctypes.c_void_p(264), ctypes.c_void_p(256), 0, 10, 0.1, None)
+    assert st == lj.LJ_ERR_ARG and b"aligned" in L.lj_last_error()
+    st = L.lj_integrate(ctypes.c_void_p(256), ctypes.c_void_p(256), 0, 10, float("nan"), None)
+    assert st == lj.LJ_ERR_ARG
+    st = L.lj_force_step_ex(ctypes.c_void_p(256), ctypes.c_void_p(256), 10, g, 0.01, 0, 0, 10, ctypes.c_void_p(256),
+                            ctypes.c_void_p(256), ctypes.c_void_p(256), 3, 0, None, None)
+    assert st == lj.LJ_ERR_ARG and b"lanes" in L.lj_last_error()
+    st = L.lj_force_step_ex(ctypes.c_void_p(256), ctypes.c_void_p(256), 10, g, 0.01, 1, 0, 10, ctypes.c_void_p(256),
+                            ctypes.c_void_p(256), ctypes.c_void_p(256), 0, 1, None, None)
+    assert st == lj.LJ_ERR_UNSUPPORTED
+    assert L.lj_wrap(None, None, 0, 0.0, None) == lj.LJ_ERR_ARG
+
+
+def test_product_binding_has_no_cpu_fallback():
+    """The product package never imports the oracle or a CPU path."""
+    pkg = os.path.join(ROOT, "paper_1806_05713_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f

@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars: neighbour lists, integrate, wrap, displacement,
+cell order -- bit-exact; momenta after a force step -- C-12 metric
+max|p_gpu - p_ref| / S <= 1e-12 (BASELINE.json north_star tolerance with the
+denominator of reading C-12); the ordered kernel -- bit-exact.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import lj_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def lj():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1806_05713_b200 import build, lj as _lj
+    build.build()
+    _lj.load()
+    return _lj
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda:0")
+
+
+def to_dev(x, dev, pad=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    from paper_1806_05713_b200 import lj as _lj
+    r = _lj.pack_aos4(t)
+    if pad is not None:
+        r[:, 3] = torch.from_numpy(pad).to(dev)
+    return r
+
+
+def from_dev(x):
+    return x[:, :3].cpu().numpy()
+
+
+def assert_same_list(gl, ol):
+    n_e = gl.n_entries
+    assert n_e == ol.n_entries
+    assert np.array_equal(gl.number_of_partners.cpu().numpy(), ol.number_of_partners)
+    assert np.array_equal(gl.pointer.cpu().numpy(), ol.pointer)
+    assert np.array_equal(gl.sorted_list[:n_e].cpu().numpy(), ol.sorted_list)
+
+
+@pytest.fixture(scope="module")
+def systems():
+    out = {1: lj_inputs.config(1), 2: lj_inputs.config(2)}
+    w3 = lj_inputs.config(3)
+    perm = oracle.cell_order(w3.q, w3.L, w3.rs)
+    w3.q = np.ascontiguousarray(w3.q[perm])
+    w3.p = np.ascontiguousarray(w3.p[perm])
+    out[3] = w3
+    return out
+
+
+# ---- lists ------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+@pytest.mark.parametrize("half", [True, False])
+def test_list_bit_exact(lj, dev, systems, cfg, half):
+    w = systems[cfg]
+    g = lj.geom(w.L, w.rc, w.rs)
+    gl = lj.build_list(to_dev(w.q, dev), g, half)
+    assert_same_list(gl, oracle.list_cells(w.q, w.L, w.rs, half))
+
+
+@pytest.mark.parametrize("rows", [(0, 1), (17, 17), (1000, 2000), (1234, 3999), (3999, 4000), (0, 4000)])
+def test_list_row_ranges(lj, dev, systems, rows):
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    gl = lj.build_list(to_dev(w.q, dev), g, False, *rows)
+    assert_same_list(gl, oracle.list_cells(w.q, w.L, w.rs, False, *rows))
+
+
+@pytest.mark.parametrize("seed,n,L", [(0, 1000, 10.0), (1, 3000, 14.0), (2, 1, 10.0), (3, 0, 10.0), (4, 5000, 9.9)])
+@pytest.mark.parametrize("half", [True, False])
+def test_list_random_gas_and_edges(lj, dev, seed, n, L, half):
+    """Dense/ragged random systems incl. nc = 3 (smallest grid), n = 1 and n = 0."""
+    q = lj_inputs.random_gas(n, L, seed)
+    g = lj.geom(L, 3.0, 3.3)
+    qd = to_dev(q.reshape(-1, 3), dev) if n else torch.empty((0, 4), dtype=torch.float64, device=dev)
+    gl = lj.build_list(qd, g, half)
+    if n:
+        assert_same_list(gl, oracle.list_cells(q, L, 3.3, half))
+    else:
+        assert gl.n_entries == 0 and gl.pointer.cpu().tolist() == [0]
+
+
+def test_list_unwrapped_positions(lj, dev, systems):
+    """Positions drifted outside [0,L) (between rebuilds): cells use wrapped coordinates."""
+    w = systems[1]
+    rng = np.random.default_rng(5)
+    q = w.q + rng.uniform(-0.15, 0.15, w.q.shape)
+    g = lj.geom(w.L, w.rc, w.rs)
+    gl = lj.build_list(to_dev(q, dev), g, False)
+    assert_same_list(gl, oracle.list_cells(q, w.L, w.rs, False))
+
+
+def test_list_capacity_protocol(lj, dev, systems):
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    L = lj.load()
+    b = ctypes.c_size_t()
+    assert L.lj_build_list_workspace(w.n, g, ctypes.byref(b)) == 0
+    ws = torch.empty(b.value, dtype=torch.uint8, device=dev)
+    npart = torch.empty(w.n, dtype=torch.int32, device=dev)
+    ptr = torch.empty(w.n + 1, dtype=torch.int64, device=dev)
+    ne = ctypes.c_int64(-1)
+    st = L.lj_build_list(lj._ptr(q), w.n, g, 1, 0, w.n, lj._ptr(npart), lj._ptr(ptr), None, 0, ctypes.byref(ne),
+                         lj._ptr(ws), ws.numel(), lj._stream())
+    assert st == lj.LJ_ERR_CAPACITY
+    assert ne.value == oracle.list_cells(w.q, w.L, w.rs, True).n_entries
+    # too-small workspace and partial half range are rejected before launching
+    st = L.lj_build_list(lj._ptr(q), w.n, g, 1, 0, w.n, lj._ptr(npart), lj._ptr(ptr), None, 0, ctypes.byref(ne),
+                         lj._ptr(ws), 16, lj._stream())
+    assert st == lj.LJ_ERR_ARG
+    st = L.lj_build_list(lj._ptr(q), w.n, g, 1, 0, 10, lj._ptr(npart), lj._ptr(ptr), None, 0, ctypes.byref(ne),
+                         lj._ptr(ws), ws.numel(), lj._stream())
+    assert st == lj.LJ_ERR_UNSUPPORTED
+
+
+def test_cell_order_and_permute(lj, dev, systems):
+    w = systems[2]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    perm = lj.cell_order(q, g)
+    assert np.array_equal(perm.cpu().numpy(), oracle.cell_order(w.q, w.L, w.rs))
+    qp = lj.permute_rows(q, perm)
+    assert np.array_equal(from_dev(qp), w.q[perm.cpu().numpy()])
+
+
+# ---- force --------------------------------------------------------------------
+
+def oracle_force(w, p0, half):
+    ol = oracle.list_cells(w.q, w.L, w.rs, half)
+    full = ol if not half else oracle.list_cells(w.q, w.L, w.rs, False)
+    return oracle.force_step(w.q, p0, w.L, w.rc, w.dt, ol), oracle.abs_contrib(w.q, p0, w.L, w.rc, w.dt, full), full
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+@pytest.mark.parametrize("half", [True, False])
+@pytest.mark.parametrize("lanes", [0, 1, 4, 8, 16, 32])
+def test_force_parity(lj, dev, systems, cfg, half, lanes):
+    w = systems[cfg]
+    rng = np.random.default_rng(cfg)
+    p0 = rng.normal(0, 1, (w.n, 3))
+    ref, S, full = oracle_force(w, p0, half)
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    gl = lj.build_list(q, g, half)
+    p = to_dev(p0, dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    lj.force_step(q, p, g, w.dt, gl, lanes_per_row=lanes, n_interactions=cnt)
+    got = from_dev(p)
+    e = oracle.parity_error(got, ref, S)
+    assert e <= TOL, f"C-12 error {e}"
+    # interactions counted = entries inside r_c (integer, exact)
+    n_in = _entries_inside(w, half)
+    assert int(cnt.item()) == n_in
+
+
+def _entries_inside(w, half):
+    ol = oracle.list_cells(w.q, w.L, w.rs, half)
+    pr = ol.pairs()
+    d = w.q[pr[:, 1]] - w.q[pr[:, 0]]
+    d = np.where(d > 0.5 * w.L, d - w.L, np.where(d < -0.5 * w.L, d + w.L, d))
+    r2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+    return int(np.count_nonzero(r2 < w.rc * w.rc))
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_ordered_kernel_bit_exact(lj, dev, systems, cfg):
+    """Pin-11: the ordered full-list kernel reproduces the oracle bit for bit."""
+    w = systems[cfg]
+    rng = np.random.default_rng(10 + cfg)
+    p0 = rng.normal(0, 1, (w.n, 3))
+    ref, _, _ = oracle_force(w, p0, False)
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    gl = lj.build_list(q, g, False)
+    p = to_dev(p0, dev)
+    lj.force_step(q, p, g, w.dt, gl, ordered=True)
+    assert np.array_equal(from_dev(p), ref)
+
+
+def test_force_row_range_partition(lj, dev, systems):
+    """Pin-12 on the GPU: per-range results concatenate to the 1-range result bit-exactly."""
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    p0 = np.random.default_rng(3).normal(0, 1, (w.n, 3))
+    whole = to_dev(p0, dev)
+    lj.force_step(q, whole, g, w.dt, lj.build_list(q, g, False))
+    parts = to_dev(p0, dev)
+    for b, e in ((0, 1333), (1333, 2667), (2667, 4000)):
+        lj.force_step(q, parts, g, w.dt, lj.build_list(q, g, False, b, e))
+    assert torch.equal(whole, parts)
+
+
+def test_padding_ignored_and_preserved(lj, dev, systems):
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    rng = np.random.default_rng(4)
+    pad_q, pad_p = rng.normal(0, 1e6, w.n), rng.normal(0, 1e6, w.n)
+    p0 = rng.normal(0, 1, (w.n, 3))
+    outs = []
+    for pq, pp in ((None, None), (pad_q, pad_p)):
+        q = to_dev(w.q, dev, pq)
+        p = to_dev(p0, dev, pp)
+        for half in (True, False):
+            lj.force_step(q, p, g, w.dt, lj.build_list(q, g, half))
+        if pq is not None:
+            assert np.array_equal(q[:, 3].cpu().numpy(), pad_q)
+            assert np.array_equal(p[:, 3].cpu().numpy(), pad_p)
+        outs.append(from_dev(p))
+    ref_half, S, _ = oracle_force(w, p0, True)
+    ref, _, _ = oracle_force(w, ref_half, False)
+    for o in outs:
+        assert oracle.parity_error(o, ref, S + np.abs(ref_half)) <= TOL
+
+
+@pytest.mark.parametrize("line", [(1.0, 24.0, 0.0), (2 ** (1 / 6), 0.0, 1e-13), (2.5, -1.55998e-2, 5e-8)])
+def test_spec_two_atom_examples(lj, dev, line):
+    """SPEC.md:56-58 through the C ABI (periodic box large enough to be open)."""
+    r, df, tol = line
+    q = np.array([[5.0, 5.0, 5.0], [5.0 + r, 5.0, 5.0]])
+    g = lj.geom(20.0, 3.0, 3.3)
+    qd = to_dev(q, dev)
+    for half in (True, False):
+        p = to_dev(np.zeros((2, 3)), dev)
+        lj.force_step(qd, p, g, 1.0, lj.build_list(qd, g, half))
+        got = from_dev(p)
+        assert abs(-got[0, 0] / r - df) <= tol
+        assert np.array_equal(got[1], -got[0])
+
+
+def test_cutoff_strict_gpu(lj, dev):
+    g = lj.geom(20.0, 3.0, 3.3)
+    for r, nonzero in ((3.0 + 1e-12, False), (3.0, False), (3.0 - 1e-12, True)):
+        q = to_dev(np.array([[5.0, 5.0, 5.0], [5.0 + r, 5.0, 5.0]]), dev)
+        for half in (True, False):
+            for ordered in ((False, True) if not half else (False,)):
+                p = to_dev(np.zeros((2, 3)), dev)
+                lj.force_step(q, p, g, 0.01, lj.build_list(q, g, half), ordered=ordered)
+                assert (from_dev(p)[0, 0] != 0.0) == nonzero
+
+
+def test_perfect_lattice_gpu(lj, dev):
+    """Pin-4: 140 partners per atom, zero force, PE/atom = lattice sum."""
+    C = 8
+    q = lj_inputs.fcc_positions(C)
+    L = lj_inputs.box_length(C)
+    g = lj.geom(L, 3.0, 3.3)
+    qd = to_dev(q, dev)
+    full = lj.build_list(qd, g, False)
+    assert torch.all(full.number_of_partners == 140)
+    p = to_dev(np.zeros_like(q), dev)
+    lj.force_step(qd, p, g, 1.0, full)
+    S = oracle.abs_contrib(q, None, L, 3.0, 1.0, oracle.list_cells(q, L, 3.3, False))
+    assert np.all(np.abs(from_dev(p)) <= 1e-13 * S)
+    e = lj.energy(qd, p, g, full).cpu().numpy()
+    assert e[1] / q.shape[0] == pytest.approx(-7.762386540408147023, rel=1e-12)
+
+
+# ---- integrate / bookkeeping / energy ---------------------------------------------
+
+def test_integrate_wrap_displacement_bit_exact(lj, dev, systems):
+    w = systems[1]
+    rng = np.random.default_rng(8)
+    p0 = rng.normal(0, 1, (w.n, 3))
+    q = to_dev(w.q, dev)
+    p = to_dev(p0, dev)
+    qref = q.clone()
+    lj.integrate(q, p, 0.37, 100, 3900)
+    ref = oracle.integrate(w.q, p0, 0.37, 100, 3900)
+    assert np.array_equal(from_dev(q), ref)
+    d = lj.max_displacement(q, qref, 50, 3950).item()
+    assert d == oracle.max_displacement(ref, w.q, 50, 3950)
+    q2 = q.clone()
+    lj.wrap(q2, w.L, qref)
+    assert np.array_equal(from_dev(q2), oracle.wrap(ref, w.L))
+    assert torch.equal(q2, qref)
+
+
+@pytest.mark.parametrize("half", [True, False])
+def test_energy(lj, dev, systems, half):
+    w = systems[1]
+    p0 = np.random.default_rng(9).normal(0, 1, (w.n, 3))
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    gl = lj.build_list(q, g, half)
+    e = lj.energy(q, to_dev(p0, dev), g, gl).cpu().numpy()
+    ke, pe = oracle.energy(w.q, p0, w.L, w.rc, oracle.list_cells(w.q, w.L, w.rs, half))
+    assert e[0] == pytest.approx(ke, rel=1e-12)
+    assert e[1] == pytest.approx(pe, rel=1e-12)
+
+
+def test_argument_errors(lj, dev, systems):
+    w = systems[1]
+    q = to_dev(w.q, dev)
+    L = lj.load()
+    bad = lj.geom(w.L, 3.3, 3.0)   # rc > rs
+    st = L.lj_force_step(lj._ptr(q), lj._ptr(q), w.n, bad, 0.01, 0, 0, w.n, None, None, None, lj._stream())
+    assert st == lj.LJ_ERR_ARG and b"rc" in L.lj_last_error()
+    g = lj.geom(w.L, w.rc, w.rs)
+    flat = torch.empty(4 * w.n + 1, dtype=torch.float64, device=dev)
+    mis = ctypes.c_void_p(flat.data_ptr() + 8)   # 8-byte aligned, not 32
+    st = L.lj_integrate(mis, lj._ptr(q), 0, 10, 0.1, lj._stream())
+    assert st == lj.LJ_ERR_ARG
+    st = L.lj_force_step(lj._ptr(q), lj._ptr(q), w.n, g, 0.01, 1, 0, 10, None, None, None, lj._stream())
+    assert st == lj.LJ_ERR_UNSUPPORTED
+    with pytest.raises(TypeError):
+        lj.integrate(q.float(), q.float(), 0.1)
+
+
+def test_kdk_step_matches_oracle(lj, dev):
+    """One velocity-Verlet (KDK) step through the ABI vs the oracle's md_run (O8)."""
+    w = lj_inputs.make_system(10, jitter_seed=1, T=1.0, mom_seed=5, dt=0.005)
+    q1, p1, _, _ = oracle.md_run(w.q, w.p, w.L, w.rc, w.rs, w.dt, 1)
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    p = to_dev(w.p, dev)
+    gl = lj.build_list(q, g, False)
+    lj.force_step(q, p, g, 0.5 * w.dt, gl)
+    lj.integrate(q, p, w.dt)
+    lj.force_step(q, p, g, 0.5 * w.dt, gl)
+    full = oracle.list_cells(w.q, w.L, w.rs, False)
+    S = oracle.abs_contrib(q1, w.p, w.L, w.rc, w.dt, full)
+    assert oracle.parity_error(from_dev(p), p1, S) <= TOL
+    # positions differ only through p_{1/2} rounding: tiny absolute error
+    assert np.abs(from_dev(q) - q1).max() < 1e-14
