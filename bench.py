@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the LJ fp64 force hot path (arXiv 1806.05713) on B200.
+
+Default workload (BASELINE.json metric "pair-interactions/sec ... at 1/2/4/8
+B200"): config 4 -- N = 2,048,000 FCC atoms, rho = 1, jitter +-0.05, Gaussian
+momenta T = 1, r_c = 3.0, r_s = 3.3, full list, rows split across ranks with a
+per-step all-gather of positions, leapfrog dt = 0.01 with bookkeeping rebuilds.
+A step = force + integrate + all-gather + displacement check (+ rebuild when
+triggered), i.e. every §8(a) row of the path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle
+(oracle/, plain C, single thread) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import lj_inputs  # noqa: E402
+
+METRIC = "LJ fp64 pair-interactions/sec (G/s) and ms/force-step at 1/2/4/8 B200"
+FLOP_PER_ENTRY = 22          # 21 add/mul + 1 division per full-list entry (no p_j update)
+FP64_LANES_PER_SM = 64       # B200: 64 FP64 lanes per SM
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--list", default=None, choices=["half", "full"], help="configs 2/3 only (default full)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---- clocks sampler (NVML, during the timed region) ------------------------------
+
+class ClockSampler:
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 -- NVML missing: report no clocks
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+        if not self.samples:
+            return None
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---- the oracle as the CPU baseline / reference arm ---------------------------------
+
+def oracle_sample(w, steps, frac=8, warmup=0, timings=None):
+    """Oracle (plain C, 1 thread) leapfrog steps on rows [0, N/frac) of the workload:
+    force + integrate + displacement check per step, list built once (not timed).
+    Returns (pairs/s, seconds, pairs)."""
+    import oracle
+    rows = w.n // frac
+    q = oracle.wrap(w.q, w.L)   # a fresh contiguous copy
+    lst = oracle.list_cells(q, w.L, w.rs, False, 0, rows)
+    p = w.p.copy()
+    qref = q.copy()
+    pairs = 0.0
+    t_total = 0.0
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        oracle.force_step(q, p, w.L, w.rc, w.dt, lst, inplace=True)
+        oracle.integrate(q, p, w.dt, 0, rows, inplace=True)
+        oracle.max_displacement(q, qref, 0, rows)
+        dt_s = time.perf_counter() - t0
+        if s >= warmup:
+            t_total += dt_s
+            if timings is not None:
+                timings.append(dt_s)
+    # interactions in the sample (entries inside r_c; each pair counted from both
+    # rows in a full list -> unique pairs = entries / 2, as for the GPU line)
+    pr = lst.pairs()
+    d = q[pr[:, 1]] - q[pr[:, 0]]
+    d = np.where(d > 0.5 * w.L, d - w.L, np.where(d < -0.5 * w.L, d + w.L, d))
+    inside = np.count_nonzero((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2] < w.rc * w.rc)
+    pairs = inside / 2.0 * steps
+    return pairs / t_total, t_total, pairs
+
+
+def cores_used():
+    return 1   # the oracle is single-threaded (PAPER.md:72 protocol)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = lj_inputs.config(args.config)
+    frac = 64 if args.config == 4 else (512 if args.config == 5 else 4)
+    step_times = []
+    t0 = time.perf_counter()
+    value, secs, pairs = oracle_sample(w, args.steps, frac=frac, warmup=args.warmup, timings=step_times)
+    sample = (f"config {args.config} rows [0, N/{frac}) = {w.n // frac} of {w.n} atoms; oracle list built once "
+              f"(untimed); {args.steps} timed leapfrog steps (force + integrate + displacement), {args.warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value / 1e9, "unit": "G pair-interactions/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}", "n_atoms": w.n, "sample_rows": w.n // frac},
+        "cpu_baseline": {"value": value / 1e9, "unit": "G pair-interactions/s", "cores": cores_used(),
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": value / 1e9, "unit": "G pair-interactions/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ----------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1806_05713_b200 import lj, md
+
+    lj.load()   # fails loudly without the CUDA library
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA GPU (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = dist.group.WORLD
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    w = lj_inputs.config(args.config)
+    g = lj.geom(w.L, w.rc, w.rs)
+    pk, pk_kind = peaks()
+    force_only = args.config in (2, 3)
+    half = (args.list == "half") if force_only else False
+    if force_only and world > 1:
+        raise SystemExit("configs 2/3 are single-GPU force-only benchmarks")
+
+    rb, re_ = md.row_range(w.n, rank, world)
+    be = md.LibBackend(w.n, g, rb, re_, dev, half=half)
+    sim = md.LeapfrogMD(be, w.q, w.p, g, w.dt, rank, world, comm)
+    if force_only:
+        if args.config == 3:   # cell-order reordering (a3) before building
+            perm = lj.cell_order(sim.q, g)
+            sim.q = lj.permute_rows(sim.q, perm)
+            sim.p = lj.permute_rows(sim.p, perm)
+            sim.lst = be.build(sim.q)
+        else:
+            sim.lst = be.build(sim.q)
+    else:
+        sim.half_kick()   # leapfrog start: p_0 -> p_{1/2}
+
+    stream = torch.cuda.current_stream()
+    f_ev = []
+
+    def one_step(record):
+        if force_only:
+            if record:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
+            if record:
+                b.record(stream)
+                f_ev.append((a, b))
+            return
+        if record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
+        if record:
+            b.record(stream)
+            f_ev.append((a, b))
+        be.integrate(sim.q, sim.p, w.dt, sim.rb, sim.re)
+        sim._allgather_q()
+        sim.check_rebuild()
+
+    for _ in range(args.warmup):
+        one_step(False)
+    sim.interactions()   # reset counter
+    reb0 = sim.stats.rebuilds
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = lj.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        one_step(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = lj.launch_count() - launches0
+    ck = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    entries_inside = sim.interactions()           # summed over ranks and timed steps
+    pairs = entries_inside if half else entries_inside / 2.0
+    value = pairs / (ms_max * 1e-3)
+    rebuilds = sim.stats.rebuilds - reb0
+    force_ms = [a.elapsed_time(b) for a, b in f_ev]
+    force_avg = sum(force_ms) / len(force_ms)
+    entries_per_launch = sim.lst.n_entries       # own rows (last list)
+
+    # ---- roofline of the dominant kernel (force), FP64 pipe ----
+    sm_mhz = pk.get("sm_max_mhz", 1965.0)
+    peak_tflops = N_SM * FP64_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    achieved = FLOP_PER_ENTRY * entries_per_launch / (force_avg * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    hbm_bytes = (4 * entries_per_launch + (re_ - rb) * (32 + 32 + 32 + 8 + 4) + w.n * 32)
+
+    # ---- e2e: same steps through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        qh = torch.empty((re_ - rb, 4), dtype=torch.float64, pin_memory=True)
+        ph = torch.empty((re_ - rb, 4), dtype=torch.float64, pin_memory=True)
+        qh.copy_(sim.q[rb:re_])
+        ph.copy_(sim.p[rb:re_])
+        sim.interactions()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            sim.q[rb:re_].copy_(qh, non_blocking=True)
+            sim.p[rb:re_].copy_(ph, non_blocking=True)
+            one_step(False)
+            qh.copy_(sim.q[rb:re_], non_blocking=True)
+            ph.copy_(sim.p[rb:re_], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e_pairs = sim.interactions()
+        e_pairs = e_pairs if half else e_pairs / 2.0
+        nbytes = 2 * (re_ - rb) * 32
+        e2e = {"value": e_pairs / (float(ems.item()) * 1e-3) / 1e9, "unit": "G pair-interactions/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "ms_per_step": float(ems.item()) / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        frac = 64 if args.config == 4 else (512 if args.config == 5 else 4)
+        v, secs, _ = oracle_sample(w, 3, frac=frac)
+        cpu = {"value": v / 1e9, "unit": "G pair-interactions/s", "cores": cores_used(), "kind": "oracle",
+               "sample": f"config {args.config} rows [0,N/{frac}) ({w.n // frac} atoms), 3 oracle leapfrog steps "
+                         f"(force+integrate+displacement, list build untimed), {secs:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value / 1e9, "unit": "G pair-interactions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config{args.config}", "n_atoms": w.n, "list": "half" if half else "full",
+                       "order": "cell" if args.config == 3 else ("shuffled" if args.config == 2 else "lattice"),
+                       "dt": w.dt, "rc": w.rc, "rs": w.rs, "parallelism": f"rows/{world}",
+                       "l2": "inputs larger than L2 (CSR list %.2f GB + records)" % (4 * sim.lst.n_entries / 1e9),
+                       "rebuilds_in_timed_steps": rebuilds},
+            "ms_per_force_step": force_avg,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tflops, "traffic": traffic,
+                         "kernel": "k_force<G,false> (full list)",
+                         "peak_kind": f"derived: {N_SM} SM x {FP64_LANES_PER_SM} FP64 lanes x 2 x {sm_mhz:.0f} MHz",
+                         "flop_per_entry": FLOP_PER_ENTRY, "entries_per_launch": entries_per_launch,
+                         "hbm_view": {"algorithmic_bytes": hbm_bytes,
+                                      "achieved_gbs": hbm_bytes / (force_avg * 1e-3) / 1e9,
+                                      "peak_gbs": pk.get("hbm_gbs"), "peak_kind": pk_kind}},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

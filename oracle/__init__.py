@@ -153,10 +153,13 @@ def cell_order(q, L, rs):
     return perm
 
 
-def force_step(q, p, L, rc, dt, csr: CSR):
-    """Alg. 3 with Alg. 1 arithmetic; returns a new p."""
+def force_step(q, p, L, rc, dt, csr: CSR, inplace=False):
+    """Alg. 3 with Alg. 1 arithmetic; returns a new p (or updates p in place)."""
     q = _f64(q)
-    p = _f64(p).copy()
+    if inplace:
+        assert p.dtype == np.float64 and p.flags.c_contiguous
+    else:
+        p = _f64(p).copy()
     lib().lj_oracle_force_step(_p(q), _p(p), q.shape[0], L, rc, dt, int(csr.half), csr.row_begin,
                                csr.row_end, _p(csr.number_of_partners), _p(csr.pointer),
                                _p(csr.sorted_list))
@@ -181,8 +184,11 @@ def abs_contrib(q, p0, L, rc, dt, csr: CSR):
     return S
 
 
-def integrate(q, p, dt, begin=0, end=None):
-    q = _f64(q).copy()
+def integrate(q, p, dt, begin=0, end=None, inplace=False):
+    if inplace:
+        assert q.dtype == np.float64 and q.flags.c_contiguous
+    else:
+        q = _f64(q).copy()
     p = _f64(p)
     lib().lj_oracle_integrate(_p(q), _p(p), begin, q.shape[0] if end is None else end, dt)
     return q

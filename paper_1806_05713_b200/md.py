@@ -1,0 +1,167 @@
+"""MD driver over the C ABI: leapfrog velocity Verlet with the bookkeeping
+rebuild (readings O8, C-16), row-split across ranks
+ with a per-step all-gather of positions.
+
+One rank per GPU.  Rank r owns atoms/rows [r N/P, (r+1) N/P): it keeps the
+replicated positions q (N AoS4 records), its own momenta p (global-indexed,
+only own rows meaningful), its own bookkeeping reference q_ref and the CSR list
+of its own rows.  Per step (SURVEY §3 call stack 4):
+
+    force(dt) on own rows          -- liblj lj_force_step (kernel)
+    integrate(dt) on own rows      -- liblj lj_integrate (kernel)
+    all-gather q                   -- torch.distributed (NCCL), P > 1 only
+    disp = max |q - q_ref| own     -- liblj lj_max_displacement (kernel)
+    all-reduce MAX disp            -- torch.distributed, P > 1 only
+    if 2 disp >= rs - rc:          -- host decision (one 8-byte readback)
+        wrap q, q_ref <- q         -- liblj lj_wrap (kernel)
+        rebuild own rows           -- liblj lj_build_list (kernels)
+
+The compute backend is injectable so the multi-rank plumbing can be tested on
+CPU with gloo (tests/test_dist_gloo.py); the product backend is LibBackend,
+which has no fallback: it raises if liblj.so or the GPU is missing.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+import torch.distributed as dist
+
+from . import lj
+
+
+def row_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows of `rank`: [rank*n//world, (rank+1)*n//world) (contiguous slabs in lattice order)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+class LibBackend:
+    """liblj.so on the current CUDA device."""
+
+    def __init__(self, n, g: lj.Geom, row_begin, row_end, device, half=False):
+        lj.load()
+        self.device = torch.device(device)
+        self.n, self.g = n, g
+        self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device)
+
+    def records(self, xyz):
+        t = xyz if isinstance(xyz, torch.Tensor) else torch.from_numpy(xyz)
+        return lj.pack_aos4(t.to(self.device, dtype=torch.float64))
+
+    def empty_records(self, n):
+        return torch.empty((n, 4), dtype=torch.float64, device=self.device)
+
+    def build(self, q):
+        return self.builder.build(q)
+
+    def force(self, q, p, dt, lst, counter=None):
+        lj.force_step(q, p, self.g, dt, lst, n_interactions=counter)
+
+    def integrate(self, q, p, dt, b, e):
+        lj.integrate(q, p, dt, b, e)
+
+    def max_disp(self, q, q_ref, b, e, out):
+        lj.max_displacement(q, q_ref, b, e, out)
+
+    def wrap(self, q, q_ref):
+        lj.wrap(q, self.g.L, q_ref)
+
+    def energy(self, q, p, lst, out):
+        lj.energy(q, p, self.g, lst, out)
+
+
+@dataclasses.dataclass
+class StepStats:
+    rebuilds: int = 0
+    steps: int = 0
+
+
+class LeapfrogMD:
+    """Row-split leapfrog MD.  `comm` is None for a single rank, else a
+    torch.distributed process group (NCCL on GPUs, gloo in CPU tests)."""
+
+    def __init__(self, backend, q_xyz, p_xyz, g: lj.Geom, dt: float, rank: int = 0, world: int = 1, comm=None,
+                 count_interactions: bool = True):
+        self.be, self.g, self.dt = backend, g, float(dt)
+        self.n = q_xyz.shape[0]
+        self.rank, self.world, self.comm = rank, world, comm
+        self.rb, self.re = row_range(self.n, rank, world)
+        self.q = backend.records(q_xyz)
+        self.p = backend.records(p_xyz)
+        self.q_ref = backend.empty_records(self.n)
+        self.disp = torch.zeros(1, dtype=torch.float64, device=self.q.device)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=self.q.device) if count_interactions else None
+        self.stats = StepStats()
+        self.margin = g.rs - g.rc
+        self.be.wrap(self.q, self.q_ref)
+        self.lst = self.be.build(self.q)
+
+    # ---- collectives (no-ops for one rank) ----
+    def _allgather_q(self):
+        if self.world > 1:
+            own = self.q[self.rb:self.re]
+            if self.n % self.world == 0:
+                # in-place all-gather: rank r's slab is already at its offset
+                dist.all_gather_into_tensor(self.q, own.clone() if self._gloo() else own, group=self.comm)
+            else:
+                parts = [self.q[slice(*row_range(self.n, r, self.world))] for r in range(self.world)]
+                dist.all_gather(parts, own.clone(), group=self.comm)
+
+    def _gloo(self):
+        return dist.get_backend(self.comm) == "gloo"
+
+    def _allreduce_max(self, t):
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.comm)
+
+    def _allreduce_sum(self, t):
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.comm)
+
+    # ---- MD ----
+    def half_kick(self):
+        """p += F(q) dt/2 -- turns p_0 into p_{1/2} (leapfrog start) or back."""
+        self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
+
+    def check_rebuild(self) -> bool:
+        self.be.max_disp(self.q, self.q_ref, self.rb, self.re, self.disp)
+        self._allreduce_max(self.disp)
+        if 2.0 * float(self.disp.item()) >= self.margin:
+            self.be.wrap(self.q, self.q_ref)
+            self.lst = self.be.build(self.q)
+            self.stats.rebuilds += 1
+            return True
+        return False
+
+    def step(self):
+        """One leapfrog step: p += F(q) dt; q += p dt; all-gather; bookkeeping."""
+        self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
+        self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
+        self._allgather_q()
+        self.check_rebuild()
+        self.stats.steps += 1
+
+    def kdk_step(self):
+        """One synchronised velocity-Verlet step (O8): kick dt/2, drift, rebuild check, kick dt/2."""
+        self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
+        self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
+        self._allgather_q()
+        self.check_rebuild()
+        self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
+        self.stats.steps += 1
+
+    def energy(self):
+        """(KE, PE) summed over ranks (p must be synchronised, e.g. after kdk_step)."""
+        out = torch.zeros(2, dtype=torch.float64, device=self.q.device)
+        self.be.energy(self.q, self.p, self.lst, out)
+        self._allreduce_sum(out)
+        return float(out[0]), float(out[1])
+
+    def interactions(self) -> int:
+        """List entries inside r_c counted by the force kernels since the last call, summed over ranks."""
+        if self.counter is None:
+            return 0
+        c = self.counter.clone()
+        self._allreduce_sum(c)
+        self.counter.zero_()
+        return int(c.item())

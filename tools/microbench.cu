@@ -1,0 +1,102 @@
+// Roofline microbenchmarks for the force kernel's denominators (SURVEY B-15):
+//   fp64_fma:     FP64 pipe issue rate (independent DFMA chains)
+//   gather_replay: the force kernel's exact access pattern with no math --
+//                  G lanes per row, index load + one 32-B record gather per
+//                  entry, summed into registers (achieved gather bandwidth)
+//   stream_list:  sequential read of the CSR index array (HBM stream)
+// Built as tools/libljmicro.so, driven by tools/microbench.py.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+struct __align__(32) rec4 {
+    double x, y, z, w;
+};
+
+__device__ __forceinline__ rec4 ldrec(const rec4* p) {
+    rec4 r;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+
+__global__ void k_fp64_fma(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+           x7 = x0 + 7;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            x0 = fma(x0, a, b);
+            x1 = fma(x1, a, b);
+            x2 = fma(x2, a, b);
+            x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b);
+            x5 = fma(x5, a, b);
+            x6 = fma(x6, a, b);
+            x7 = fma(x7, a, b);
+        }
+    }
+    double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678) out[0] = s;
+}
+
+template <int G>
+__global__ void k_gather(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
+                         const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* out) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t r = t / G;
+    int g = threadIdx.x % G;
+    double s = 0;
+    if (r < rows) {
+        const int32_t* l = list + ptr[r];
+        int n = npart[r];
+        int k = g;
+        for (; k + G < n; k += 2 * G) {
+            int j0 = __ldg(l + k), j1 = __ldg(l + k + G);
+            rec4 a = ldrec(q + j0), b = ldrec(q + j1);
+            s += a.x + a.y + a.z + b.x + b.y + b.z;
+        }
+        if (k < n) {
+            rec4 a = ldrec(q + __ldg(l + k));
+            s += a.x + a.y + a.z;
+        }
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
+__global__ void k_stream(const int4* __restrict__ a, int64_t n4, int* out) {
+    int acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        int4 v = __ldg(a + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345678) out[0] = acc;
+}
+
+extern "C" {
+
+int mb_fp64_fma(double* out, int blocks, int threads, int iters, void* stream) {
+    k_fp64_fma<<<blocks, threads, 0, (cudaStream_t)stream>>>(out, iters, 0.999999, 1e-7);
+    return (int)cudaGetLastError();
+}
+
+int mb_gather(const double* q, int64_t rows, const int32_t* npart, const int64_t* ptr, const int32_t* list,
+              double* out, int G, void* stream) {
+    int64_t threads = rows * G;
+    unsigned grid = (unsigned)((threads + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    const rec4* qq = (const rec4*)q;
+    switch (G) {
+        case 1: k_gather<1><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        case 2: k_gather<2><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        case 4: k_gather<4><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        case 8: k_gather<8><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        case 16: k_gather<16><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        default: return -1;
+    }
+    return (int)cudaGetLastError();
+}
+
+int mb_stream(const void* a, int64_t bytes, int* out, void* stream) {
+    k_stream<<<148 * 16, 256, 0, (cudaStream_t)stream>>>((const int4*)a, bytes / 16, out);
+    return (int)cudaGetLastError();
+}
+}
