@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--list", default=None, choices=["half", "full"], help="configs 2/3 only (default full)")
+    ap.add_argument("--order", default=None, choices=["lattice", "shuffled", "cell"],
+                    help="storage order; default: config 2 shuffled, 3 cell, 4/5 cell (re-sorted at every rebuild)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -210,18 +212,11 @@ def main():
     if force_only and world > 1:
         raise SystemExit("configs 2/3 are single-GPU force-only benchmarks")
 
+    order = args.order or {2: "shuffled", 3: "cell"}.get(args.config, "cell")
     rb, re_ = md.row_range(w.n, rank, world)
     be = md.LibBackend(w.n, g, rb, re_, dev, half=half)
-    sim = md.LeapfrogMD(be, w.q, w.p, g, w.dt, rank, world, comm)
-    if force_only:
-        if args.config == 3:   # cell-order reordering (a3) before building
-            perm = lj.cell_order(sim.q, g)
-            sim.q = lj.permute_rows(sim.q, perm)
-            sim.p = lj.permute_rows(sim.p, perm)
-            sim.lst = be.build(sim.q)
-        else:
-            sim.lst = be.build(sim.q)
-    else:
+    sim = md.LeapfrogMD(be, w.q, w.p, g, w.dt, rank, world, comm, reorder=(order == "cell"))
+    if not force_only:
         sim.half_kick()   # leapfrog start: p_0 -> p_{1/2}
 
     stream = torch.cuda.current_stream()
@@ -336,7 +331,7 @@ def main():
             "higher_is_better": True, "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config{args.config}", "n_atoms": w.n, "list": "half" if half else "full",
-                       "order": "cell" if args.config == 3 else ("shuffled" if args.config == 2 else "lattice"),
+                       "order": order + (" (re-sorted at every rebuild)" if order == "cell" and not force_only else ""),
                        "dt": w.dt, "rc": w.rc, "rs": w.rs, "parallelism": f"rows/{world}",
                        "l2": "inputs larger than L2 (CSR list %.2f GB + records)" % (4 * sim.lst.n_entries / 1e9),
                        "rebuilds_in_timed_steps": rebuilds},

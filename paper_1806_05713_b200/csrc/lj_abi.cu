@@ -121,7 +121,7 @@ lj_status lj_build_list_workspace(int64_t n, lj_geom g, size_t* bytes) {
     LJ_TRY(check_geom(g, true));
     if (!bytes) return fail(LJ_ERR_ARG, "workspace: null output");
     CellGrid cg = make_grid(g);
-    *bytes = build_workspace_layout(n, cg.ncell, n).total;
+    *bytes = build_workspace_layout(n, cg.ncell, n).total;   // sized for all rows
     return LJ_OK;
 }
 
@@ -145,25 +145,29 @@ lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)workspace;
     const int64_t rows = row_end - row_begin;
-    const double rs2 = g.rs * g.rs;
     LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
     if (rows > 0)
-        LJ_CUDA(launch_list_count(q, n, cg, rs2, half, row_begin, row_end, number_of_partners, ws, W, s),
-                "lj_build_list/count");
+        LJ_CUDA(launch_list_pass1(cg, g.rs, half, row_begin, row_end, number_of_partners, ws, W, s),
+                "lj_build_list/pass1");
     LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, pointer, rows, (int64_t*)(ws + W.off_scan), W.scan_blocks, s),
             "lj_build_list/scan");
     int64_t total = 0;
+    int32_t row_overflow = 0;
     LJ_CUDA(cudaMemcpyAsync(&total, pointer + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
             "lj_build_list/readback");
+    if (rows > 0)
+        LJ_CUDA(cudaMemcpyAsync(&row_overflow, list_row_overflow_flag(ws, W), sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                s),
+                "lj_build_list/readback");
     LJ_CUDA(cudaStreamSynchronize(s), "lj_build_list/sync");
     *n_entries = total;
     if (total > capacity)
         return fail(LJ_ERR_CAPACITY, "build_list: capacity %lld < required %lld", (long long)capacity,
                     (long long)total);
     if (rows > 0 && total > 0)
-        LJ_CUDA(launch_list_fill(q, n, cg, rs2, half, row_begin, row_end, number_of_partners, pointer, sorted_list,
-                                 ws, W, s),
-                "lj_build_list/fill");
+        LJ_CUDA(launch_list_pass2(cg, g.rs, half, row_begin, row_end, number_of_partners, pointer, sorted_list,
+                                  row_overflow != 0, ws, W, s),
+                "lj_build_list/pass2");
     return LJ_OK;
 }
 
@@ -207,10 +211,16 @@ lj_status lj_force_step_ex(const double* q, double* p, int64_t n, lj_geom g, dou
     if (rows > 0 && (!q || !p || !number_of_partners || !pointer))
         return fail(LJ_ERR_ARG, "force: null pointer");
     if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "force: q/p not 32-byte aligned");
-    int lanes = lanes_per_row;
-    if (lanes == 0) lanes = half ? 8 : 8;
+    int lanes = lanes_per_row & 0xff, unroll = lanes_per_row >> 8;
+    if (lanes == 0) {   // defaults from the round-1 sweep (profiles/r01_sweep_*.jsonl)
+        lanes = 8;
+        if (unroll == 0) unroll = half ? 2 : 4;
+    }
     if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
         return fail(LJ_ERR_ARG, "force: lanes_per_row must be 0,1,2,4,8,16 or 32 (got %d)", lanes_per_row);
+    if (unroll != 0 && unroll != 2 && unroll != 4)
+        return fail(LJ_ERR_ARG, "force: unroll (lanes_per_row >> 8) must be 0, 2 or 4 (got %d)", unroll);
+    lanes |= unroll << 8;
     ForceArgs a;
     a.q = q;
     a.p = p;

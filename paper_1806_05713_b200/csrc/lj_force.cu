@@ -97,8 +97,10 @@ __device__ __forceinline__ void count_interactions(unsigned cnt, unsigned long l
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(n_inter, v);
 }
 
-// Full list: G lanes per row, no atomics, p_i committed once by lane 0 of the group.
-template <int G, bool HALF>
+// G lanes per row, U independent partner gathers in flight per lane.
+// Full list: no atomics, p_i committed once by lane 0 of the group.
+// Half list: p_j += df r by fp64 REDs, p_i committed by REDs as well.
+template <int G, int U, bool HALF>
 __global__ void __launch_bounds__(kForceThreads)
     k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
             const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
@@ -114,48 +116,30 @@ __global__ void __launch_bounds__(kForceThreads)
         const rec4 qi = load_rec(q, i);
         const int32_t* __restrict__ lst = list + ptr[r];
         const int n = npart[r];
-        int k = g;
-        for (; k + G < n; k += 2 * G) {
-            const int j0 = __ldg(lst + k), j1 = __ldg(lst + k + G);
-            const rec4 q0 = load_rec(q, j0), q1 = load_rec(q, j1);
-            double dx0, dy0, dz0, dx1, dy1, dz1;
-            bool in0, in1;
-            double df0 = pair_df(qi, q0, c, dx0, dy0, dz0, in0);
-            double df1 = pair_df(qi, q1, c, dx1, dy1, dz1, in1);
-            ax = fma(-df0, dx0, ax);
-            ay = fma(-df0, dy0, ay);
-            az = fma(-df0, dz0, az);
-            ax = fma(-df1, dx1, ax);
-            ay = fma(-df1, dy1, ay);
-            az = fma(-df1, dz1, az);
-            cnt += in0 + in1;
-            if (HALF) {
-                if (in0) {
-                    atomicAdd(&p[j0].x, df0 * dx0);
-                    atomicAdd(&p[j0].y, df0 * dy0);
-                    atomicAdd(&p[j0].z, df0 * dz0);
+        for (int k0 = g; k0 < n; k0 += U * G) {
+            int j[U];
+            rec4 qj[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) j[u] = (k0 + u * G < n) ? __ldg(lst + k0 + u * G) : -1;
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (j[u] >= 0) qj[u] = load_rec(q, j[u]);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (j[u] >= 0) {
+                    double dx, dy, dz;
+                    bool in;
+                    const double df = pair_df(qi, qj[u], c, dx, dy, dz, in);
+                    ax = fma(-df, dx, ax);
+                    ay = fma(-df, dy, ay);
+                    az = fma(-df, dz, az);
+                    cnt += in;
+                    if (HALF && in) {
+                        atomicAdd(&p[j[u]].x, df * dx);
+                        atomicAdd(&p[j[u]].y, df * dy);
+                        atomicAdd(&p[j[u]].z, df * dz);
+                    }
                 }
-                if (in1) {
-                    atomicAdd(&p[j1].x, df1 * dx1);
-                    atomicAdd(&p[j1].y, df1 * dy1);
-                    atomicAdd(&p[j1].z, df1 * dz1);
-                }
-            }
-        }
-        if (k < n) {
-            const int j0 = __ldg(lst + k);
-            const rec4 q0 = load_rec(q, j0);
-            double dx0, dy0, dz0;
-            bool in0;
-            double df0 = pair_df(qi, q0, c, dx0, dy0, dz0, in0);
-            ax = fma(-df0, dx0, ax);
-            ay = fma(-df0, dy0, ay);
-            az = fma(-df0, dz0, az);
-            cnt += in0;
-            if (HALF && in0) {
-                atomicAdd(&p[j0].x, df0 * dx0);
-                atomicAdd(&p[j0].y, df0 * dy0);
-                atomicAdd(&p[j0].z, df0 * dz0);
             }
         }
     }
@@ -246,7 +230,7 @@ PairConsts make_consts(const ForceArgs& a) {
     return c;
 }
 
-template <bool HALF>
+template <bool HALF, int U>
 cudaError_t launch_g(const ForceArgs& a, int lanes, cudaStream_t s) {
     if (a.rows <= 0) return cudaSuccess;
     PairConsts c = make_consts(a);
@@ -255,7 +239,7 @@ cudaError_t launch_g(const ForceArgs& a, int lanes, cudaStream_t s) {
     const rec4* q = (const rec4*)a.q;
     rec4* p = (rec4*)a.p;
 #define LJ_LAUNCH(G)                                                                                        \
-    k_force<G, HALF><<<grid, kForceThreads, 0, s>>>(q, p, a.row_begin, a.rows, a.npart, a.ptr, a.list, c, \
+    k_force<G, U, HALF><<<grid, kForceThreads, 0, s>>>(q, p, a.row_begin, a.rows, a.npart, a.ptr, a.list, c, \
                                                      a.n_inter)
     switch (lanes) {
         case 1: LJ_LAUNCH(1); break;
@@ -273,8 +257,18 @@ cudaError_t launch_g(const ForceArgs& a, int lanes, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t launch_force_full(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_g<false>(a, lanes, s); }
-cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_g<true>(a, lanes, s); }
+// lanes encodes G (1..32) and, in its upper bits, the unroll U (lanes = G | (U << 8); U in {2, 4}, default 2).
+template <bool HALF>
+cudaError_t launch_gu(const ForceArgs& a, int lanes, cudaStream_t s) {
+    const int U = lanes >> 8;
+    const int G = lanes & 0xff;
+    if (U == 4) return launch_g<HALF, 4>(a, G, s);
+    if (U == 0 || U == 2) return launch_g<HALF, 2>(a, G, s);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_force_full(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_gu<false>(a, lanes, s); }
+cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_gu<true>(a, lanes, s); }
 
 cudaError_t launch_force_ordered(const ForceArgs& a, cudaStream_t s) {
     if (a.rows <= 0) return cudaSuccess;

@@ -28,9 +28,13 @@ namespace {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
-constexpr int kRowBuf = 512;     // per-warp row buffer (entries); longer rows take the slow path
+}  // namespace
+constexpr int kRowCap = 192;     // v2: scratch entries per row (longer rows -> direct second pass)
+namespace {
+constexpr int kRowBuf = 512;     // fallback: per-warp row buffer (entries)
 constexpr int kCellBuf = 256;    // per-warp cell buffer for the in-cell sort
 constexpr int kListWarps = 8;
+constexpr int kMaxCand = 2048;   // v2: candidates staged per cell in shared memory
 
 __device__ __forceinline__ double min_image(double d, double L, double halfL) {
     if (L > 0.0) {
@@ -81,6 +85,8 @@ __device__ void warp_bitonic_sort(int* buf, int P, int lane) {
     }
 }
 
+__device__ __forceinline__ bool half_ok(int half, int i, int j) { return half ? (j > i) : (j != i); }
+
 __device__ __forceinline__ int next_pow2(int x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -110,8 +116,16 @@ __global__ void k_cell_scatter(int64_t n, const int32_t* __restrict__ cell_of, c
 }
 
 // One warp per cell: sort the cell's atoms ascending, then gather q into cell order.
-__global__ void k_cell_sort_gather(const rec4* __restrict__ q, int64_t ncell, const int64_t* __restrict__ start,
-                                   int32_t* __restrict__ atoms, rec4* __restrict__ q_cell) {
+__device__ __forceinline__ double wrap_exact(double x, double L) {
+    double xw = __dsub_rn(x, __dmul_rn(L, floor(__ddiv_rn(x, L))));
+    if (xw >= L) xw = __dsub_rn(xw, L);
+    return xw;
+}
+
+__global__ void k_cell_sort_gather(const rec4* __restrict__ q, CellGrid cg, const int64_t* __restrict__ start,
+                                   int32_t* __restrict__ atoms, rec4* __restrict__ q_cell,
+                                   float4* __restrict__ qf_cell) {
+    const int64_t ncell = cg.ncell;
     __shared__ int buf[kListWarps][kCellBuf];
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int64_t c = blockIdx.x * (int64_t)kListWarps + w; c < ncell; c += (int64_t)gridDim.x * kListWarps) {
@@ -135,133 +149,317 @@ __global__ void k_cell_sort_gather(const rec4* __restrict__ q, int64_t ncell, co
             }
         }
         __syncwarp();
-        for (int k = lane; k < cnt; k += 32) q_cell[s + k] = q[atoms[s + k]];
+        for (int k = lane; k < cnt; k += 32) {
+            const rec4 r = q[atoms[s + k]];
+            q_cell[s + k] = r;
+            qf_cell[s + k] = make_float4((float)wrap_exact(r.x, cg.L), (float)wrap_exact(r.y, cg.L),
+                                         (float)wrap_exact(r.z, cg.L), 0.0f);
+        }
     }
 }
 
 // ---- list ----------------------------------------------------------------
 
-struct Stencil {
-    int64_t s[27];
-    int n[27];
-};
-
-__device__ __forceinline__ void neighbour_cells(int c, const CellGrid& cg, const int64_t* __restrict__ start,
-                                                int64_t* s, int* cnt) {
-    int nc = cg.nc;
-    int cz = c % nc, cy = (c / nc) % nc, cx = c / (nc * nc);
-    int t = 0;
-    for (int dx = -1; dx <= 1; dx++)
-        for (int dy = -1; dy <= 1; dy++)
-            for (int dz = -1; dz <= 1; dz++) {
-                int x = cx + dx, y = cy + dy, z = cz + dz;
-                x += (x < 0) ? nc : 0;
-                x -= (x >= nc) ? nc : 0;
-                y += (y < 0) ? nc : 0;
-                y -= (y >= nc) ? nc : 0;
-                z += (z < 0) ? nc : 0;
-                z -= (z >= nc) ? nc : 0;
-                int cc = (x * nc + y) * nc + z;
-                s[t] = start[cc];
-                cnt[t] = (int)(start[cc + 1] - s[t]);
-                t++;
-            }
+// Neighbour cell t (0..26) of cell c: start, count and the periodic shift that
+// places its atoms (wrapped coordinates) next to cell c (float screen only).
+__device__ __forceinline__ int neighbour_cell(int c, int t, const CellGrid& cg, const int64_t* __restrict__ start,
+                                              int64_t& s, int& cnt, float& sx, float& sy, float& sz) {
+    const int nc = cg.nc;
+    const int cz = c % nc, cy = (c / nc) % nc, cx = c / (nc * nc);
+    int x = cx + t / 9 - 1, y = cy + (t / 3) % 3 - 1, z = cz + t % 3 - 1;
+    const float L = (float)cg.L;
+    sx = x < 0 ? -L : (x >= nc ? L : 0.0f);
+    sy = y < 0 ? -L : (y >= nc ? L : 0.0f);
+    sz = z < 0 ? -L : (z >= nc ? L : 0.0f);
+    x += (x < 0) ? nc : 0;
+    x -= (x >= nc) ? nc : 0;
+    y += (y < 0) ? nc : 0;
+    y -= (y >= nc) ? nc : 0;
+    z += (z < 0) ? nc : 0;
+    z -= (z >= nc) ? nc : 0;
+    const int cc = (x * nc + y) * nc + z;
+    if (start) {
+        s = start[cc];
+        cnt = (int)(start[cc + 1] - s);
+    }
+    return cc;
 }
 
-template <bool FILL>
-__global__ void __launch_bounds__(kListWarps * 32)
-    k_list(const rec4* __restrict__ q_cell, const int32_t* __restrict__ atoms, const int64_t* __restrict__ start,
-           int64_t ncell, CellGrid cg, double rs2, int half, int64_t row_begin, int64_t row_end,
-           int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, int32_t* __restrict__ list) {
+struct ListArgs {
+    const rec4* q_cell;       // positions in cell order (raw, for the exact test)
+    const float4* qf_cell;    // wrapped positions in cell order, fp32 (screen only)
+    const int32_t* atoms;     // cell order -> atom index
+    const int64_t* start;     // cell -> first slot (ncell + 1)
+    int64_t ncell;
+    CellGrid cg;
+    double rs2;               // rs*rs, the oracle's constant
+    float rs2_screen;         // conservative fp32 screen radius^2 (> rs2 + max fp32 error)
+    int half;
+    int64_t row_begin, row_end;
+    int32_t* npart;           // [rows]
+    const int64_t* ptr;       // [rows+1] (direct mode)
+    int32_t* out;             // scratch [rows * kRowCap] or list
+    int32_t* overflow_cells;  // cells with more than kMaxCand candidates
+    int32_t* n_overflow;      // [0] = #overflow cells, [1] = row overflow flag
+};
+
+// Exact accept test of the queued candidate slot s (bit-identical to the oracle)
+// and in-order append of the accepted j to dst.
+__device__ __forceinline__ void exact_flush(const ListArgs& a, const unsigned long long* key, const int* Gi, int s,
+                                            bool valid, const rec4& qi, double L, double halfL, int32_t* dst,
+                                            int64_t cap, int& cursor, int lane) {
+    bool acc = false;
+    int j = 0;
+    if (valid) {
+        const unsigned long long k = key[s];
+        const int m = (int)(k & 0xffffffffull);
+        j = (int)(k >> 32);
+        const rec4 qj = a.q_cell[Gi[m]];
+        acc = dist2_exact(qi, qj, L, halfL) < a.rs2;
+    }
+    const unsigned msk = __ballot_sync(0xffffffffu, acc);
+    const int pos = cursor + __popc(msk & ((1u << lane) - 1u));
+    if (acc && pos < cap) dst[pos] = j;
+    cursor += __popc(msk);
+}
+
+// Builder v2: one CTA per cell.  The 27 neighbour cells' atoms (M candidates)
+// are staged in shared memory, sorted by atom index ONCE per cell (so that
+// every row of the cell comes out ascending without a per-row sort), then one
+// warp per row scans them: fp32 screen on 32 candidates at a time -> in-order
+// queue of survivors -> exact fp64 test 32 survivors at a time -> ballot
+// compaction straight into the row's output.
+template <int DIRECT>
+__global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
+    float4* A = reinterpret_cast<float4*>(smem + kMaxCand * 8);
+    int* Gi = reinterpret_cast<int*>(smem + kMaxCand * 24);
+    int* qbuf = reinterpret_cast<int*>(smem + kMaxCand * 28);
     __shared__ int64_t s_start[27];
-    __shared__ int s_cnt[27];
-    __shared__ int rowbuf[FILL ? kListWarps : 1][FILL ? kRowBuf : 1];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const double L = cg.L, halfL = 0.5 * cg.L;
-    for (int64_t c = blockIdx.x; c < ncell; c += gridDim.x) {
-        int64_t cs = start[c];
-        int ccnt = (int)(start[c + 1] - cs);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int64_t s[27];
-            int cn[27];
-            neighbour_cells((int)c, cg, start, s, cn);
-            for (int t = 0; t < 27; t++) {
-                s_start[t] = s[t];
-                s_cnt[t] = cn[t];
+    __shared__ int s_off[28];
+    __shared__ float s_shift[27][3];
+    __shared__ int s_any;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const double L = a.cg.L, halfL = 0.5 * a.cg.L;
+    int* myq = qbuf + w * 64;
+    for (int64_t c = blockIdx.x; c < a.ncell; c += gridDim.x) {
+        const int64_t cs = a.start[c];
+        const int ccnt = (int)(a.start[c + 1] - cs);
+        __syncthreads();   // smem of the previous cell no longer in use
+        if (tid == 0) s_any = 0;
+        if (tid < 27) {
+            // slot of neighbour tid in ascending cell-id order (cell ids are distinct, nc >= 3)
+            int64_t st;
+            int cn;
+            float sx, sy, sz;
+            const int my = neighbour_cell((int)c, tid, a.cg, a.start, st, cn, sx, sy, sz);
+            int rank = 0;
+            for (int u = 0; u < 27; u++) {
+                int64_t su;
+                int cu;
+                float fx, fy, fz;
+                rank += neighbour_cell((int)c, u, a.cg, nullptr, su, cu, fx, fy, fz) < my;
             }
+            s_start[rank] = st;
+            s_off[rank + 1] = cn;
+            s_shift[rank][0] = sx;
+            s_shift[rank][1] = sy;
+            s_shift[rank][2] = sz;
         }
         __syncthreads();
-        for (int t = w; t < ccnt; t += kListWarps) {
-            int i = atoms[cs + t];
-            if (i < row_begin || i >= row_end) continue;
-            rec4 qi = q_cell[cs + t];
-            int64_t r = i - row_begin;
-            if (!FILL) {
-                int count = 0;
-                for (int nb = 0; nb < 27; nb++) {
-                    int64_t s2 = s_start[nb];
-                    int n2 = s_cnt[nb];
-                    for (int k = lane; k < n2; k += 32) {
-                        int j = atoms[s2 + k];
-                        rec4 qj = q_cell[s2 + k];
-                        bool ok = half ? (j > i) : (j != i);
-                        if (ok && dist2_exact(qi, qj, L, halfL) < rs2) count++;
-                    }
+        for (int t = tid; t < ccnt; t += blockDim.x) {
+            const int i = a.atoms[cs + t];
+            if (i >= a.row_begin && i < a.row_end) s_any = 1;
+        }
+        if (tid == 0) {
+            s_off[0] = 0;
+            for (int t = 0; t < 27; t++) s_off[t + 1] += s_off[t];
+        }
+        __syncthreads();
+        if (!s_any) continue;
+        const int M = s_off[27];
+        if (M > kMaxCand) {
+            if (!DIRECT && tid == 0) {
+                int k = atomicAdd(&a.n_overflow[0], 1);
+                a.overflow_cells[k] = (int)c;
+            }
+            continue;
+        }
+        const int P = next_pow2(M > 0 ? M : 1);
+        for (int m = tid; m < P; m += blockDim.x) {
+            if (m < M) {
+                int lo = 0, hi = 27;   // largest t with s_off[t] <= m
+                while (hi - lo > 1) {
+                    int mid = (lo + hi) >> 1;
+                    if (s_off[mid] <= m) lo = mid; else hi = mid;
                 }
-                for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
-                if (lane == 0) npart[r] = count;
+                const int64_t g = s_start[lo] + (m - s_off[lo]);
+                const int j = a.atoms[g];
+                float4 f = a.qf_cell[g];
+                f.x += s_shift[lo][0];
+                f.y += s_shift[lo][1];
+                f.z += s_shift[lo][2];
+                A[m] = f;
+                Gi[m] = (int)g;
+                key[m] = ((unsigned long long)(unsigned)j << 32) | (unsigned)m;
             } else {
-                int cnt = npart[r];
-                int64_t base = ptr[r];
-                int* buf = rowbuf[w];
-                bool fits = cnt <= kRowBuf;
-                int cursor = 0;
-                for (int nb = 0; nb < 27; nb++) {
-                    int64_t s2 = s_start[nb];
-                    int n2 = s_cnt[nb];
-                    for (int k0 = 0; k0 < n2; k0 += 32) {
-                        int k = k0 + lane;
-                        bool acc = false;
-                        int j = -1;
-                        if (k < n2) {
-                            j = atoms[s2 + k];
-                            rec4 qj = q_cell[s2 + k];
-                            bool ok = half ? (j > i) : (j != i);
-                            acc = ok && dist2_exact(qi, qj, L, halfL) < rs2;
-                        }
-                        unsigned m = __ballot_sync(0xffffffffu, acc);
-                        int pos = cursor + __popc(m & ((1u << lane) - 1u));
-                        if (acc) {
-                            if (fits)
-                                buf[pos] = j;
-                            else
-                                list[base + pos] = j;
-                        }
-                        cursor += __popc(m);
-                    }
-                }
-                __syncwarp();
-                if (fits) {
-                    int P = next_pow2(cnt);
-                    for (int k = cnt + lane; k < P; k += 32) buf[k] = INT_MAX;
-                    __syncwarp();
-                    warp_bitonic_sort(buf, P, lane);
-                    for (int k = lane; k < cnt; k += 32) list[base + k] = buf[k];
-                    __syncwarp();
-                } else if (lane == 0) {   // very long row: insertion sort in global memory
-                    for (int a = 1; a < cnt; a++) {
-                        int v = list[base + a], b = a - 1;
-                        while (b >= 0 && list[base + b] > v) {
-                            list[base + b + 1] = list[base + b];
-                            b--;
-                        }
-                        list[base + b + 1] = v;
-                    }
-                }
-                __syncwarp();
+                key[m] = ~0ull;
             }
         }
+        __syncthreads();
+        // Adaptive: with atoms stored in cell order the staged keys are already
+        // ascending (neighbour cells staged in ascending cell id) -> no sort.
+        int unsorted = 0;
+        for (int m = tid; m + 1 < M; m += blockDim.x) unsorted |= key[m] > key[m + 1];
+        if (__syncthreads_or(unsorted))
+        for (int k = 2; k <= P; k <<= 1) {   // block bitonic sort of the staged keys
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int idx = tid; idx < P; idx += blockDim.x) {
+                    const int ixj = idx ^ j;
+                    if (ixj > idx) {
+                        const unsigned long long x = key[idx], y = key[ixj];
+                        if ((x > y) == ((idx & k) == 0)) {
+                            key[idx] = y;
+                            key[ixj] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int t = w; t < ccnt; t += kListWarps) {
+            const int i = a.atoms[cs + t];
+            if (i < a.row_begin || i >= a.row_end) continue;
+            const int64_t r = i - a.row_begin;
+            const rec4 qi = a.q_cell[cs + t];
+            const float4 fi = a.qf_cell[cs + t];
+            int32_t* dst;
+            int64_t cap;
+            if (DIRECT) {
+                dst = a.out + a.ptr[r];
+                cap = LLONG_MAX;
+            } else {
+                dst = a.out + r * (int64_t)kRowCap;
+                cap = kRowCap;
+            }
+            int cursor = 0, qn = 0;
+            for (int s0 = 0; s0 < M; s0 += 32) {
+                const int s = s0 + lane;
+                bool pass = false;
+                if (s < M) {
+                    const unsigned long long k = key[s];
+                    const int j = (int)(k >> 32);
+                    const float4 f = A[(int)(k & 0xffffffffull)];
+                    const float dx = f.x - fi.x, dy = f.y - fi.y, dz = f.z - fi.z;
+                    pass = half_ok(a.half, i, j) && (dx * dx + dy * dy + dz * dz < a.rs2_screen);
+                }
+                const unsigned msk = __ballot_sync(0xffffffffu, pass);
+                if (pass) myq[qn + __popc(msk & ((1u << lane) - 1u))] = s;
+                qn += __popc(msk);
+                __syncwarp();
+                if (qn >= 32) {
+                    exact_flush(a, key, Gi, myq[lane], true, qi, L, halfL, dst, cap, cursor, lane);
+                    const int rest = lane < qn - 32 ? myq[32 + lane] : 0;
+                    __syncwarp();
+                    if (lane < qn - 32) myq[lane] = rest;
+                    qn -= 32;
+                    __syncwarp();
+                }
+            }
+            if (qn > 0) exact_flush(a, key, Gi, lane < qn ? myq[lane] : 0, lane < qn, qi, L, halfL, dst, cap,
+                                    cursor, lane);
+            __syncwarp();
+            if (lane == 0) {
+                if (!DIRECT) {
+                    a.npart[r] = cursor;
+                    if (cursor > kRowCap) atomicOr(&a.n_overflow[1], 1);
+                }
+            }
+        }
+    }
+}
+
+// Fallback for cells with more than kMaxCand candidates (dense or tiny boxes):
+// one warp per row straight from global memory, per-row bitonic sort.
+template <int DIRECT>
+__global__ void __launch_bounds__(kListWarps * 32) k_list_fallback(ListArgs a) {
+    __shared__ int rowbuf[kListWarps][kRowBuf];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const double L = a.cg.L, halfL = 0.5 * a.cg.L;
+    const int nover = a.n_overflow[0];
+    for (int oc = blockIdx.x; oc < nover; oc += gridDim.x) {
+        const int c = a.overflow_cells[oc];
+        const int64_t cs = a.start[c];
+        const int ccnt = (int)(a.start[c + 1] - cs);
+        for (int t = w; t < ccnt; t += kListWarps) {
+            const int i = a.atoms[cs + t];
+            if (i < a.row_begin || i >= a.row_end) continue;
+            const int64_t r = i - a.row_begin;
+            const rec4 qi = a.q_cell[cs + t];
+            int* buf = rowbuf[w];
+            int cursor = 0;
+            int32_t* gdst = DIRECT ? a.out + a.ptr[r] : nullptr;
+            for (int nb = 0; nb < 27; nb++) {
+                int64_t s2;
+                int n2;
+                float sx, sy, sz;
+                neighbour_cell(c, nb, a.cg, a.start, s2, n2, sx, sy, sz);
+                for (int k0 = 0; k0 < n2; k0 += 32) {
+                    const int k = k0 + lane;
+                    bool acc = false;
+                    int j = -1;
+                    if (k < n2) {
+                        j = a.atoms[s2 + k];
+                        acc = half_ok(a.half, i, j) && dist2_exact(qi, a.q_cell[s2 + k], L, halfL) < a.rs2;
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, acc);
+                    const int pos = cursor + __popc(m & ((1u << lane) - 1u));
+                    if (acc) {
+                        if (pos < kRowBuf) buf[pos] = j;
+                        if (DIRECT) gdst[pos] = j;
+                    }
+                    cursor += __popc(m);
+                }
+            }
+            __syncwarp();
+            if (cursor <= kRowBuf) {
+                const int P = next_pow2(cursor > 0 ? cursor : 1);
+                for (int k = cursor + lane; k < P; k += 32) buf[k] = INT_MAX;
+                __syncwarp();
+                warp_bitonic_sort(buf, P, lane);
+                int32_t* dst = DIRECT ? gdst : a.out + r * (int64_t)kRowCap;
+                const int lim = DIRECT ? cursor : min(cursor, kRowCap);
+                for (int k = lane; k < lim; k += 32) dst[k] = buf[k];
+            } else if (DIRECT && lane == 0) {   // very long row: insertion sort in place
+                for (int x = 1; x < cursor; x++) {
+                    int v = gdst[x], y = x - 1;
+                    while (y >= 0 && gdst[y] > v) {
+                        gdst[y + 1] = gdst[y];
+                        y--;
+                    }
+                    gdst[y + 1] = v;
+                }
+            }
+            __syncwarp();
+            if (lane == 0 && !DIRECT) {
+                a.npart[r] = cursor;
+                if (cursor > kRowCap) atomicOr(&a.n_overflow[1], 1);
+            }
+        }
+    }
+}
+
+// scratch rows (stride kRowCap) -> CSR, one warp per row
+__global__ void k_compact(const int32_t* __restrict__ scratch, const int32_t* __restrict__ npart,
+                          const int64_t* __restrict__ ptr, int64_t rows, int32_t* __restrict__ list) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int c = npart[r];
+        const int32_t* src = scratch + r * (int64_t)kRowCap;
+        int32_t* dst = list + ptr[r];
+        for (int k = lane; k < c; k += 32) dst[k] = src[k];
     }
 }
 
@@ -376,10 +574,14 @@ BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows) {
     o = align256(o + sizeof(int32_t) * (size_t)n);
     W.off_qcell = o;
     o = align256(o + sizeof(rec4) * (size_t)n);
+    W.off_qf = o;
+    o = align256(o + sizeof(float4) * (size_t)n);
     W.off_scan = o;
     o = align256(o + sizeof(int64_t) * (size_t)(W.scan_blocks + 1));
-    W.off_misc = o;
-    o = align256(o + 64);
+    W.off_over = o;    // [0] overflow cell count, [1] row overflow flag, then ncell cell ids
+    o = align256(o + sizeof(int32_t) * (size_t)(ncell + 2));
+    W.off_scratch = o; // rows * kRowCap int32
+    o = align256(o + sizeof(int32_t) * (size_t)rows * kRowCap);
     W.total = o;
     return W;
 }
@@ -404,6 +606,7 @@ cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* w
     int32_t* cursor = (int32_t*)(ws + W.off_cursor);
     int32_t* atoms = (int32_t*)(ws + W.off_atoms);
     rec4* q_cell = (rec4*)(ws + W.off_qcell);
+    float4* qf_cell = (float4*)(ws + W.off_qf);
     int64_t* scan = (int64_t*)(ws + W.off_scan);
     cudaError_t e;
     if ((e = cudaMemsetAsync(count, 0, sizeof(int32_t) * (size_t)cg.ncell, s)) != cudaSuccess) return e;
@@ -415,40 +618,80 @@ cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* w
     if ((e = launch_scan_i32_to_i64(count, start, cg.ncell, scan, W.scan_blocks, s)) != cudaSuccess) return e;
     if (n > 0) {
         k_cell_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, cell_of, start, cursor, atoms);
-        k_cell_sort_gather<<<grid_for(cg.ncell, kListWarps), kListWarps * 32, 0, s>>>((const rec4*)q, cg.ncell, start,
-                                                                                     atoms, q_cell);
+        k_cell_sort_gather<<<grid_for(cg.ncell, kListWarps), kListWarps * 32, 0, s>>>((const rec4*)q, cg, start,
+                                                                                     atoms, q_cell, qf_cell);
         g_launches += 2;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_list_count(const double* q, int64_t n, const CellGrid& cg, double rs2, int half,
-                              int64_t row_begin, int64_t row_end, int32_t* npart, char* ws,
-                              const BuildWorkspace& W, cudaStream_t s) {
-    (void)q;
-    (void)n;
-    const int32_t* atoms = (const int32_t*)(ws + W.off_atoms);
-    const rec4* q_cell = (const rec4*)(ws + W.off_qcell);
-    const int64_t* start = (const int64_t*)(ws + W.off_start);
-    int grid = (int)(cg.ncell < 148 * 16 ? cg.ncell : 148 * 16);
-    k_list<false><<<grid, kListWarps * 32, 0, s>>>(q_cell, atoms, start, cg.ncell, cg, rs2, half, row_begin, row_end,
-                                                   npart, nullptr, nullptr);
-    g_launches++;
+static ListArgs list_args(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end, int32_t* npart,
+                          const int64_t* ptr, int32_t* out, char* ws, const BuildWorkspace& W) {
+    ListArgs a;
+    a.q_cell = (const rec4*)(ws + W.off_qcell);
+    a.qf_cell = (const float4*)(ws + W.off_qf);
+    a.atoms = (const int32_t*)(ws + W.off_atoms);
+    a.start = (const int64_t*)(ws + W.off_start);
+    a.ncell = cg.ncell;
+    a.cg = cg;
+    a.rs2 = rs * rs;
+    // fp32 screen: positions (|x| <= L) carry <= ~2 ulp(L) = 2.4e-7 L error per axis;
+    // widen the radius by 8e-7 L + 1e-5 so every exact pair passes the screen.
+    double rsc = rs + 8e-7 * cg.L + 1e-5;
+    a.rs2_screen = (float)(rsc * rsc);
+    a.half = half;
+    a.row_begin = row_begin;
+    a.row_end = row_end;
+    a.npart = npart;
+    a.ptr = ptr;
+    a.out = out;
+    a.n_overflow = (int32_t*)(ws + W.off_over);
+    a.overflow_cells = a.n_overflow + 2;
+    return a;
+}
+
+static int list_grid(const CellGrid& cg, int per_sm) {
+    int64_t g = 148 * per_sm;
+    return (int)(cg.ncell < g ? cg.ncell : g);
+}
+
+constexpr size_t kListSmem = (size_t)kMaxCand * 28 + kListWarps * 64 * sizeof(int);
+
+cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
+                              int32_t* npart, char* ws, const BuildWorkspace& W, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_list_v2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_list_v2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, nullptr, (int32_t*)(ws + W.off_scratch), ws, W);
+    cudaError_t e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    k_list_v2<0><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+    k_list_fallback<0><<<148, kListWarps * 32, 0, s>>>(a);
+    g_launches += 2;
     return cudaGetLastError();
 }
 
-cudaError_t launch_list_fill(const double* q, int64_t n, const CellGrid& cg, double rs2, int half,
-                             int64_t row_begin, int64_t row_end, const int32_t* npart, const int64_t* ptr,
-                             int32_t* list, char* ws, const BuildWorkspace& W, cudaStream_t s) {
-    (void)q;
-    (void)n;
-    const int32_t* atoms = (const int32_t*)(ws + W.off_atoms);
-    const rec4* q_cell = (const rec4*)(ws + W.off_qcell);
-    const int64_t* start = (const int64_t*)(ws + W.off_start);
-    int grid = (int)(cg.ncell < 148 * 16 ? cg.ncell : 148 * 16);
-    k_list<true><<<grid, kListWarps * 32, 0, s>>>(q_cell, atoms, start, cg.ncell, cg, rs2, half, row_begin, row_end,
-                                                  const_cast<int32_t*>(npart), ptr, list);
-    g_launches++;
+const int32_t* list_row_overflow_flag(char* ws, const BuildWorkspace& W) { return (const int32_t*)(ws + W.off_over) + 1; }
+
+cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
+                              int32_t* npart, const int64_t* ptr, int32_t* list, bool row_overflow, char* ws,
+                              const BuildWorkspace& W, cudaStream_t s) {
+    const int64_t rows = row_end - row_begin;
+    if (!row_overflow) {
+        k_compact<<<grid_for(rows * 32, 256, 148 * 32), 256, 0, s>>>((const int32_t*)(ws + W.off_scratch), npart, ptr,
+                                                                     rows, list);
+        g_launches++;
+        return cudaGetLastError();
+    }
+    ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, ptr, list, ws, W);
+    k_list_v2<1><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+    k_list_fallback<1><<<148, kListWarps * 32, 0, s>>>(a);
+    g_launches += 2;
     return cudaGetLastError();
 }
 

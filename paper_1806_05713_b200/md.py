@@ -54,6 +54,17 @@ class LibBackend:
     def build(self, q):
         return self.builder.build(q)
 
+    def cell_order(self, q):
+        """perm[new] = old (stable sort by cell id), using the builder's workspace."""
+        perm = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        ws = self.builder.workspace
+        lj._check(lj.load().lj_cell_order(lj._ptr(q), self.n, self.g, lj._ptr(perm), lj._ptr(ws), ws.numel(),
+                                          lj._stream()))
+        return perm
+
+    def permute(self, src, perm, dst):
+        lj._check(lj.load().lj_permute_rows(lj._ptr(src), lj._ptr(dst), lj._ptr(perm), self.n, lj._stream()))
+
     def force(self, q, p, dt, lst, counter=None):
         lj.force_step(q, p, self.g, dt, lst, n_interactions=counter)
 
@@ -81,7 +92,7 @@ class LeapfrogMD:
     torch.distributed process group (NCCL on GPUs, gloo in CPU tests)."""
 
     def __init__(self, backend, q_xyz, p_xyz, g: lj.Geom, dt: float, rank: int = 0, world: int = 1, comm=None,
-                 count_interactions: bool = True):
+                 count_interactions: bool = True, reorder: bool = True):
         self.be, self.g, self.dt = backend, g, float(dt)
         self.n = q_xyz.shape[0]
         self.rank, self.world, self.comm = rank, world, comm
@@ -93,19 +104,37 @@ class LeapfrogMD:
         self.counter = torch.zeros(1, dtype=torch.int64, device=self.q.device) if count_interactions else None
         self.stats = StepStats()
         self.margin = g.rs - g.rc
-        self.be.wrap(self.q, self.q_ref)
-        self.lst = self.be.build(self.q)
+        # storage slot -> original atom id, carried in the pad lane of p (the driver
+        # owns p; every kernel ignores and preserves pads)
+        self.reorder = reorder
+        self.p[:, 3] = torch.arange(self.n, dtype=torch.float64, device=self.p.device)
+        if reorder:
+            self.q_alt = backend.empty_records(self.n)
+            self.p_alt = backend.empty_records(self.n)
+        self._rebuild()
 
     # ---- collectives (no-ops for one rank) ----
-    def _allgather_q(self):
+    def _allgather(self, x):
+        """Replicate the own-row slab of x (n records) on every rank."""
         if self.world > 1:
-            own = self.q[self.rb:self.re]
+            own = x[self.rb:self.re]
             if self.n % self.world == 0:
                 # in-place all-gather: rank r's slab is already at its offset
-                dist.all_gather_into_tensor(self.q, own.clone() if self._gloo() else own, group=self.comm)
+                dist.all_gather_into_tensor(x, own.clone() if self._gloo() else own, group=self.comm)
             else:
-                parts = [self.q[slice(*row_range(self.n, r, self.world))] for r in range(self.world)]
-                dist.all_gather(parts, own.clone(), group=self.comm)
+                # uneven slabs: gather equal-size padded slabs, then scatter them back
+                m = -(-self.n // self.world)
+                send = torch.zeros((m, x.shape[1]), dtype=x.dtype, device=x.device)
+                send[: self.re - self.rb] = own
+                buf = torch.empty((self.world * m, x.shape[1]), dtype=x.dtype, device=x.device)
+                dist.all_gather_into_tensor(buf, send, group=self.comm)
+                for r in range(self.world):
+                    b, e = row_range(self.n, r, self.world)
+                    if r != self.rank:
+                        x[b:e] = buf[r * m: r * m + (e - b)]
+
+    def _allgather_q(self):
+        self._allgather(self.q)
 
     def _gloo(self):
         return dist.get_backend(self.comm) == "gloo"
@@ -123,12 +152,30 @@ class LeapfrogMD:
         """p += F(q) dt/2 -- turns p_0 into p_{1/2} (leapfrog start) or back."""
         self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
 
+    def _rebuild(self):
+        """Wrap, (optionally) re-sort the atoms into cell order (§8(a) a3), snapshot
+        q_ref and rebuild the own-row list (§8(a) a2-a4)."""
+        if self.reorder:
+            if self.world > 1:
+                self._allgather(self.p)          # momenta of all rows, to follow the permutation
+            self.be.wrap(self.q, None)
+            perm = self.be.cell_order(self.q)
+            self.be.permute(self.q, perm, self.q_alt)
+            self.be.permute(self.p, perm, self.p_alt)
+            self.q, self.q_alt = self.q_alt, self.q
+            self.p, self.p_alt = self.p_alt, self.p
+        self.be.wrap(self.q, self.q_ref)
+        self.lst = self.be.build(self.q)
+
+    def atom_ids(self):
+        """Original atom id of every storage slot (int64, device)."""
+        return self.p[:, 3].to(torch.int64)
+
     def check_rebuild(self) -> bool:
         self.be.max_disp(self.q, self.q_ref, self.rb, self.re, self.disp)
         self._allreduce_max(self.disp)
         if 2.0 * float(self.disp.item()) >= self.margin:
-            self.be.wrap(self.q, self.q_ref)
-            self.lst = self.be.build(self.q)
+            self._rebuild()
             self.stats.rebuilds += 1
             return True
         return False
