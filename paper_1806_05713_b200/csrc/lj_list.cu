@@ -205,16 +205,14 @@ struct ListArgs {
 
 // Exact accept test of the queued candidate slot s (bit-identical to the oracle)
 // and in-order append of the accepted j to dst.
-__device__ __forceinline__ void exact_flush(const ListArgs& a, const unsigned long long* key, const int* Gi, int s,
-                                            bool valid, const rec4& qi, double L, double halfL, int32_t* dst,
-                                            int64_t cap, int& cursor, int lane) {
+__device__ __forceinline__ void exact_flush(const ListArgs& a, const float4* A, const int* Gi, int s, bool valid,
+                                            const rec4& qi, double L, double halfL, int32_t* dst, int64_t cap,
+                                            int& cursor, int lane) {
     bool acc = false;
     int j = 0;
     if (valid) {
-        const unsigned long long k = key[s];
-        const int m = (int)(k & 0xffffffffull);
-        j = (int)(k >> 32);
-        const rec4 qj = a.q_cell[Gi[m]];
+        j = __float_as_int(A[s].w);
+        const rec4 qj = a.q_cell[Gi[s]];
         acc = dist2_exact(qi, qj, L, halfL) < a.rs2;
     }
     const unsigned msk = __ballot_sync(0xffffffffu, acc);
@@ -224,17 +222,18 @@ __device__ __forceinline__ void exact_flush(const ListArgs& a, const unsigned lo
 }
 
 // Builder v2: one CTA per cell.  The 27 neighbour cells' atoms (M candidates)
-// are staged in shared memory, sorted by atom index ONCE per cell (so that
-// every row of the cell comes out ascending without a per-row sort), then one
-// warp per row scans them: fp32 screen on 32 candidates at a time -> in-order
-// queue of survivors -> exact fp64 test 32 survivors at a time -> ballot
-// compaction straight into the row's output.
-template <int DIRECT>
+// are staged in shared memory in ascending atom-index order (sorted once per
+// cell, and not at all when the atoms are stored in cell order), so every row
+// of the cell comes out ascending without a per-row sort.  One warp per row
+// then scans them: fp32 screen on 32 candidates at a time -> in-order queue of
+// survivors -> exact fp64 test 32 survivors at a time -> ballot compaction
+// straight into the row's output.
+template <int DIRECT, int HALF>
 __global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
-    float4* A = reinterpret_cast<float4*>(smem + kMaxCand * 8);
-    int* Gi = reinterpret_cast<int*>(smem + kMaxCand * 24);
+    float4* A = reinterpret_cast<float4*>(smem + kMaxCand * 8);       // sorted: wrapped+shifted pos, w = j bits
+    int* Gi = reinterpret_cast<int*>(smem + kMaxCand * 24);            // sorted: slot in q_cell
     int* qbuf = reinterpret_cast<int*>(smem + kMaxCand * 28);
     __shared__ int64_t s_start[27];
     __shared__ int s_off[28];
@@ -286,48 +285,63 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
             }
             continue;
         }
-        const int P = next_pow2(M > 0 ? M : 1);
-        for (int m = tid; m < P; m += blockDim.x) {
-            if (m < M) {
-                int lo = 0, hi = 27;   // largest t with s_off[t] <= m
-                while (hi - lo > 1) {
-                    int mid = (lo + hi) >> 1;
-                    if (s_off[mid] <= m) lo = mid; else hi = mid;
-                }
-                const int64_t g = s_start[lo] + (m - s_off[lo]);
-                const int j = a.atoms[g];
-                float4 f = a.qf_cell[g];
-                f.x += s_shift[lo][0];
-                f.y += s_shift[lo][1];
-                f.z += s_shift[lo][2];
-                A[m] = f;
-                Gi[m] = (int)g;
-                key[m] = ((unsigned long long)(unsigned)j << 32) | (unsigned)m;
-            } else {
-                key[m] = ~0ull;
+        // stage the keys (j << 32 | staging slot)
+        for (int m = tid; m < M; m += blockDim.x) {
+            int lo = 0, hi = 27;   // largest t with s_off[t] <= m
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_off[mid] <= m) lo = mid; else hi = mid;
             }
+            const int j = a.atoms[s_start[lo] + (m - s_off[lo])];
+            key[m] = ((unsigned long long)(unsigned)j << 32) | (unsigned)m;
         }
         __syncthreads();
         // Adaptive: with atoms stored in cell order the staged keys are already
         // ascending (neighbour cells staged in ascending cell id) -> no sort.
         int unsorted = 0;
         for (int m = tid; m + 1 < M; m += blockDim.x) unsorted |= key[m] > key[m + 1];
-        if (__syncthreads_or(unsorted))
-        for (int k = 2; k <= P; k <<= 1) {   // block bitonic sort of the staged keys
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int idx = tid; idx < P; idx += blockDim.x) {
-                    const int ixj = idx ^ j;
-                    if (ixj > idx) {
-                        const unsigned long long x = key[idx], y = key[ixj];
-                        if ((x > y) == ((idx & k) == 0)) {
-                            key[idx] = y;
-                            key[ixj] = x;
+        if (__syncthreads_or(unsorted)) {
+            const int P = next_pow2(M);
+            for (int m = M + tid; m < P; m += blockDim.x) key[m] = ~0ull;
+            __syncthreads();
+            for (int k = 2; k <= P; k <<= 1) {   // block bitonic sort of the staged keys
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int idx = tid; idx < P; idx += blockDim.x) {
+                        const int ixj = idx ^ j;
+                        if (ixj > idx) {
+                            const unsigned long long x = key[idx], y = key[ixj];
+                            if ((x > y) == ((idx & k) == 0)) {
+                                key[idx] = y;
+                                key[ixj] = x;
+                            }
                         }
                     }
+                    __syncthreads();
                 }
-                __syncthreads();
             }
         }
+        // candidates in sorted order; pad to a multiple of 32 with far-away sentinels
+        const int M32 = (M + 31) & ~31;
+        for (int s = tid; s < M32; s += blockDim.x) {
+            if (s < M) {
+                const unsigned long long k = key[s];
+                const int m = (int)(k & 0xffffffffull);
+                int lo = 0, hi = 27;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_off[mid] <= m) lo = mid; else hi = mid;
+                }
+                const int64_t g = s_start[lo] + (m - s_off[lo]);
+                const float4 f = a.qf_cell[g];
+                A[s] = make_float4(f.x + s_shift[lo][0], f.y + s_shift[lo][1], f.z + s_shift[lo][2],
+                                   __int_as_float((int)(k >> 32)));
+                Gi[s] = (int)g;
+            } else {
+                A[s] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(-1));
+                Gi[s] = 0;
+            }
+        }
+        __syncthreads();
         for (int t = w; t < ccnt; t += kListWarps) {
             const int i = a.atoms[cs + t];
             if (i < a.row_begin || i >= a.row_end) continue;
@@ -344,37 +358,31 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
                 cap = kRowCap;
             }
             int cursor = 0, qn = 0;
-            for (int s0 = 0; s0 < M; s0 += 32) {
-                const int s = s0 + lane;
-                bool pass = false;
-                if (s < M) {
-                    const unsigned long long k = key[s];
-                    const int j = (int)(k >> 32);
-                    const float4 f = A[(int)(k & 0xffffffffull)];
-                    const float dx = f.x - fi.x, dy = f.y - fi.y, dz = f.z - fi.z;
-                    pass = half_ok(a.half, i, j) && (dx * dx + dy * dy + dz * dz < a.rs2_screen);
-                }
+            const unsigned lt = (1u << lane) - 1u;
+            for (int s = lane; s < M32; s += 32) {
+                const float4 f = A[s];
+                const int j = __float_as_int(f.w);
+                const float dx = f.x - fi.x, dy = f.y - fi.y, dz = f.z - fi.z;
+                const bool pass = (HALF ? (j > i) : (j != i)) && (dx * dx + dy * dy + dz * dz < a.rs2_screen);
                 const unsigned msk = __ballot_sync(0xffffffffu, pass);
-                if (pass) myq[qn + __popc(msk & ((1u << lane) - 1u))] = s;
+                if (pass) myq[qn + __popc(msk & lt)] = s;
                 qn += __popc(msk);
-                __syncwarp();
                 if (qn >= 32) {
-                    exact_flush(a, key, Gi, myq[lane], true, qi, L, halfL, dst, cap, cursor, lane);
+                    __syncwarp();
+                    exact_flush(a, A, Gi, myq[lane], true, qi, L, halfL, dst, cap, cursor, lane);
                     const int rest = lane < qn - 32 ? myq[32 + lane] : 0;
                     __syncwarp();
                     if (lane < qn - 32) myq[lane] = rest;
                     qn -= 32;
-                    __syncwarp();
                 }
             }
-            if (qn > 0) exact_flush(a, key, Gi, lane < qn ? myq[lane] : 0, lane < qn, qi, L, halfL, dst, cap,
-                                    cursor, lane);
             __syncwarp();
-            if (lane == 0) {
-                if (!DIRECT) {
-                    a.npart[r] = cursor;
-                    if (cursor > kRowCap) atomicOr(&a.n_overflow[1], 1);
-                }
+            if (qn > 0) exact_flush(a, A, Gi, lane < qn ? myq[lane] : 0, lane < qn, qi, L, halfL, dst, cap, cursor,
+                                    lane);
+            __syncwarp();
+            if (lane == 0 && !DIRECT) {
+                a.npart[r] = cursor;
+                if (cursor > kRowCap) atomicOr(&a.n_overflow[1], 1);
             }
         }
     }
@@ -661,16 +669,20 @@ cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t r
                               int32_t* npart, char* ws, const BuildWorkspace& W, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_list_v2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_list_v2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
-        if (e != cudaSuccess) return e;
+        void (*fns[4])(ListArgs) = {k_list_v2<0, 0>, k_list_v2<0, 1>, k_list_v2<1, 0>, k_list_v2<1, 1>};
+        for (auto f : fns) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
+            if (e != cudaSuccess) return e;
+        }
         attr = true;
     }
     ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, nullptr, (int32_t*)(ws + W.off_scratch), ws, W);
     cudaError_t e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
-    k_list_v2<0><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+    if (half)
+        k_list_v2<0, 1><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+    else
+        k_list_v2<0, 0><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
     k_list_fallback<0><<<148, kListWarps * 32, 0, s>>>(a);
     g_launches += 2;
     return cudaGetLastError();
@@ -689,7 +701,10 @@ cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t r
         return cudaGetLastError();
     }
     ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, ptr, list, ws, W);
-    k_list_v2<1><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+    if (half)
+        k_list_v2<1, 1><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+    else
+        k_list_v2<1, 0><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
     k_list_fallback<1><<<148, kListWarps * 32, 0, s>>>(a);
     g_launches += 2;
     return cudaGetLastError();

@@ -29,12 +29,13 @@ def timeit(fn, reps=20, warm=3):
 
 def main():
     dev = torch.device("cuda:0")
-    cfgs = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["2", "3", "4"])]
-    for c in cfgs:
+    cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["2", "3", "4", "4c"]
+    for cname in cfgs:
+        c = int(cname[0])
         w = lj_inputs.config(c)
         g = lj.geom(w.L, w.rc, w.rs)
         q = lj.pack_aos4(torch.from_numpy(w.q).to(dev))
-        if c == 3:
+        if c == 3 or cname.endswith("c"):
             perm = lj.cell_order(q, g)
             q = lj.permute_rows(q, perm)
         p = lj.pack_aos4(torch.from_numpy(w.p).to(dev))
@@ -46,16 +47,16 @@ def main():
             lj.force_step(q, p, g, w.dt, lst, n_interactions=cnt)
             inter = int(cnt.item())
             pairs = inter if half else inter // 2
-            print(json.dumps(dict(cfg=c, half=half, what="build", ms=round(t_build, 4), entries=lst.n_entries)),
+            print(json.dumps(dict(cfg=cname, half=half, what="build", ms=round(t_build, 4), entries=lst.n_entries)),
                   flush=True)
             for lanes in (4, 8, 16, 32, 4 | 512, 8 | 1024, 16 | 1024, 8 | 512):
                 ms = timeit(lambda: lj.force_step(q, p, g, w.dt, lst, lanes_per_row=lanes))
-                print(json.dumps(dict(cfg=c, half=half, what="force", lanes=lanes, ms=round(ms, 4),
+                print(json.dumps(dict(cfg=cname, half=half, what="force", lanes=lanes, ms=round(ms, 4),
                                       G_entries_s=round(lst.n_entries / ms / 1e6, 2),
                                       G_pairs_s=round(pairs / ms / 1e6, 2))), flush=True)
             if not half:
                 ms = timeit(lambda: lj.force_step(q, p, g, w.dt, lst, ordered=True), reps=5)
-                print(json.dumps(dict(cfg=c, half=half, what="force_ordered", ms=round(ms, 4))), flush=True)
+                print(json.dumps(dict(cfg=cname, half=half, what="force_ordered", ms=round(ms, 4))), flush=True)
         del q, p
         torch.cuda.empty_cache()
 
