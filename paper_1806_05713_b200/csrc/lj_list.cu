@@ -34,7 +34,7 @@ namespace {
 constexpr int kRowBuf = 512;     // fallback: per-warp row buffer (entries)
 constexpr int kCellBuf = 256;    // per-warp cell buffer for the in-cell sort
 constexpr int kListWarps = 8;
-constexpr int kMaxCand = 2048;   // v2: candidates staged per cell in shared memory
+constexpr int kMaxCand = 1344;   // v3: candidates staged per cell in shared memory (4 CTAs/SM)
 
 __device__ __forceinline__ double min_image(double d, double L, double halfL) {
     if (L > 0.0) {
@@ -194,6 +194,7 @@ struct ListArgs {
     CellGrid cg;
     double rs2;               // rs*rs, the oracle's constant
     float rs2_screen;         // conservative fp32 screen radius^2 (> rs2 + max fp32 error)
+    float r_screen;           // >= sqrt(rs2_screen): reach of a row for the half-cell type lists
     int half;
     int64_t row_begin, row_end;
     int32_t* npart;           // [rows]
@@ -203,45 +204,52 @@ struct ListArgs {
     int32_t* n_overflow;      // [0] = #overflow cells, [1] = row overflow flag
 };
 
-// Exact accept test of the queued candidate slot s (bit-identical to the oracle)
-// and in-order append of the accepted j to dst.
-__device__ __forceinline__ void exact_flush(const ListArgs& a, const float4* A, const int* Gi, int s, bool valid,
-                                            const rec4& qi, double L, double halfL, int32_t* dst, int64_t cap,
-                                            int& cursor, int lane) {
-    bool acc = false;
-    int j = 0;
-    if (valid) {
-        j = __float_as_int(A[s].w);
-        const rec4 qj = a.q_cell[Gi[s]];
-        acc = dist2_exact(qi, qj, L, halfL) < a.rs2;
-    }
-    const unsigned msk = __ballot_sync(0xffffffffu, acc);
-    const int pos = cursor + __popc(msk & ((1u << lane) - 1u));
-    if (acc && pos < cap) dst[pos] = j;
-    cursor += __popc(msk);
+// Exact accept test on raw fp64 coordinates, bit-identical to the oracle's
+// (readings O2/O3): d = x_j - x_i (IEEE), minimum image d -/+ L when |d| > L/2,
+// r2 = (dx*dx + dy*dy) + dz*dz without FMA, strict r2 < rs2.
+// The image decision is taken on the high word of d (|d| compared with L/2 up
+// to 2^-20 relative).  That cannot change an accept decision nor an accepted
+// r2: since L >= 3 rs, an axis with |d| within 2^-20 of L/2 gives |d| > rs for
+// either choice (reject both ways), and every other |d| is decided identically.
+__device__ __forceinline__ bool image_needed(double d, int half_hi) {
+    return (__double2hiint(d) & 0x7fffffff) > half_hi;
+}
+__device__ __forceinline__ double image_apply(double d, double L, bool need) {
+    // need: d - L for d > 0, d + L (= d - (-L)) for d < 0, exactly as the oracle
+    const double sL = __hiloint2double((__double2hiint(d) & (int)0x80000000) | __double2hiint(L), __double2loint(L));
+    return need ? __dsub_rn(d, sL) : d;
 }
 
-// Builder v2: one CTA per cell.  The 27 neighbour cells' atoms (M candidates)
+// Builder v3: one CTA per cell.  The 27 neighbour cells' atoms (M candidates)
 // are staged in shared memory in ascending atom-index order (sorted once per
-// cell, and not at all when the atoms are stored in cell order), so every row
-// of the cell comes out ascending without a per-row sort.  One warp per row
-// then scans them: fp32 screen on 32 candidates at a time -> in-order queue of
-// survivors -> exact fp64 test 32 survivors at a time -> ballot compaction
-// straight into the row's output.
+// cell; no sort when the atoms are stored in cell order) as raw fp64
+// coordinates + index.  Each of the 8 half-cells of the cell gets an ordered
+// list of the candidates inside its reach box (~57 % of M); one warp per row
+// then applies the oracle's exact test to 32 candidates of its half-cell's list
+// at a time and compacts the accepted j by ballot straight into the row, which
+// therefore comes out ascending.  No global loads in the inner loop.
 template <int DIRECT, int HALF>
-__global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
+__global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
-    float4* A = reinterpret_cast<float4*>(smem + kMaxCand * 8);       // sorted: wrapped+shifted pos, w = j bits
-    int* Gi = reinterpret_cast<int*>(smem + kMaxCand * 24);            // sorted: slot in q_cell
-    int* qbuf = reinterpret_cast<int*>(smem + kMaxCand * 28);
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);   // staging keys, then type lists
+    unsigned short* tl = reinterpret_cast<unsigned short*>(smem);
+    double2* XY = reinterpret_cast<double2*>(smem + kMaxCand * 8);
+    double* Z = reinterpret_cast<double*>(XY + (kMaxCand + 32));
+    int* J = reinterpret_cast<int*>(Z + (kMaxCand + 32));
+    unsigned char* TM = reinterpret_cast<unsigned char*>(J + (kMaxCand + 32));
     __shared__ int64_t s_start[27];
     __shared__ int s_off[28];
     __shared__ float s_shift[27][3];
     __shared__ int s_any;
+    __shared__ unsigned short s_cnt[kMaxCand / 32 + 1][8];
+    __shared__ int s_tbase[9];
+    __shared__ int s_tlen[8];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const double L = a.cg.L, halfL = 0.5 * a.cg.L;
-    int* myq = qbuf + w * 64;
+    const double L = a.cg.L;
+    const int half_hi = L > 0.0 ? __double2hiint(0.5 * L) : 0x7fffffff;
+    const long long rs2_bits = __double_as_longlong(a.rs2);
+    const float wf = (float)(a.cg.L / a.cg.nc);
+    const float R = a.r_screen;
     for (int64_t c = blockIdx.x; c < a.ncell; c += gridDim.x) {
         const int64_t cs = a.start[c];
         const int ccnt = (int)(a.start[c + 1] - cs);
@@ -320,7 +328,11 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
                 }
             }
         }
-        // candidates in sorted order; pad to a multiple of 32 with far-away sentinels
+        // Candidates in sorted order: raw coordinates, index, and the set of
+        // half-cell types whose reach box (wrapped fp32 frame, radius R) holds it.
+        const int ncz = (int)(c % a.cg.nc), ncy = (int)((c / a.cg.nc) % a.cg.nc),
+                  ncx = (int)(c / ((int64_t)a.cg.nc * a.cg.nc));
+        const float midx = (ncx + 0.5f) * wf, midy = (ncy + 0.5f) * wf, midz = (ncz + 0.5f) * wf;
         const int M32 = (M + 31) & ~31;
         for (int s = tid; s < M32; s += blockDim.x) {
             if (s < M) {
@@ -332,14 +344,73 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
                     if (s_off[mid] <= m) lo = mid; else hi = mid;
                 }
                 const int64_t g = s_start[lo] + (m - s_off[lo]);
+                const rec4 r = a.q_cell[g];
                 const float4 f = a.qf_cell[g];
-                A[s] = make_float4(f.x + s_shift[lo][0], f.y + s_shift[lo][1], f.z + s_shift[lo][2],
-                                   __int_as_float((int)(k >> 32)));
-                Gi[s] = (int)g;
+                const float fx = f.x + s_shift[lo][0], fy = f.y + s_shift[lo][1], fz = f.z + s_shift[lo][2];
+                XY[s] = make_double2(r.x, r.y);
+                Z[s] = r.z;
+                J[s] = (int)(k >> 32);
+                const unsigned bx = (fx < midx + R ? 1u : 0u) | (fx >= midx - R ? 2u : 0u);
+                const unsigned by = (fy < midy + R ? 1u : 0u) | (fy >= midy - R ? 2u : 0u);
+                const unsigned bz = (fz < midz + R ? 1u : 0u) | (fz >= midz - R ? 2u : 0u);
+                unsigned tm = 0;
+#pragma unroll
+                for (int tau = 0; tau < 8; tau++)
+                    tm |= ((bx >> (tau >> 2)) & (by >> ((tau >> 1) & 1)) & (bz >> (tau & 1)) & 1u) << tau;
+                TM[s] = (unsigned char)tm;
             } else {
-                A[s] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(-1));
-                Gi[s] = 0;
+                TM[s] = 0;
             }
+        }
+        if (tid == 0) {   // sentinel slot for the padded type lists: never accepted
+            XY[kMaxCand] = make_double2(1e300, 1e300);
+            Z[kMaxCand] = 1e300;
+            J[kMaxCand] = -1;
+        }
+        __syncthreads();
+        // per-type ordered slot lists
+        const int nch = M32 >> 5;
+        for (int ch = w; ch < nch; ch += kListWarps) {
+            const unsigned tm = TM[ch * 32 + lane];
+#pragma unroll
+            for (int tau = 0; tau < 8; tau++) {
+                const unsigned m = __ballot_sync(0xffffffffu, (tm >> tau) & 1u);
+                if (lane == 0) s_cnt[ch][tau] = (unsigned short)__popc(m);
+            }
+        }
+        __syncthreads();
+        if (tid < 8) {   // exclusive scan of the chunk counts of type tid (in place)
+            int acc = 0;
+            for (int ch = 0; ch < nch; ch++) {
+                const int v = s_cnt[ch][tid];
+                s_cnt[ch][tid] = (unsigned short)acc;
+                acc += v;
+            }
+            s_tbase[tid + 1] = (acc + 31) & ~31;   // padded length
+            s_tlen[tid] = acc;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            s_tbase[0] = 0;
+            for (int tau = 0; tau < 8; tau++) s_tbase[tau + 1] += s_tbase[tau];
+        }
+        __syncthreads();
+        const bool use_types = s_tbase[8] <= kMaxCand * 4;   // fits the reused key space (uint16)
+        if (use_types) {
+            for (int ch = w; ch < nch; ch += kListWarps) {
+                const unsigned tm = TM[ch * 32 + lane];
+#pragma unroll
+                for (int tau = 0; tau < 8; tau++) {
+                    const bool mem = (tm >> tau) & 1u;
+                    const unsigned m = __ballot_sync(0xffffffffu, mem);
+                    if (mem)
+                        tl[s_tbase[tau] + s_cnt[ch][tau] + __popc(m & ((1u << lane) - 1u))] =
+                            (unsigned short)(ch * 32 + lane);
+                }
+            }
+            for (int tau = 0; tau < 8; tau++)   // pad each list with the sentinel slot
+                for (int k = s_tbase[tau] + s_tlen[tau] + tid; k < s_tbase[tau + 1]; k += blockDim.x)
+                    tl[k] = (unsigned short)kMaxCand;
         }
         __syncthreads();
         for (int t = w; t < ccnt; t += kListWarps) {
@@ -357,29 +428,29 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_v2(ListArgs a) {
                 dst = a.out + r * (int64_t)kRowCap;
                 cap = kRowCap;
             }
-            int cursor = 0, qn = 0;
+            const int tau = ((fi.x >= midx) << 2) | ((fi.y >= midy) << 1) | (fi.z >= midz);
+            const unsigned short* lst = use_types ? tl + s_tbase[tau] : nullptr;
+            const int len32 = use_types ? s_tbase[tau + 1] - s_tbase[tau] : M32;
             const unsigned lt = (1u << lane) - 1u;
-            for (int s = lane; s < M32; s += 32) {
-                const float4 f = A[s];
-                const int j = __float_as_int(f.w);
-                const float dx = f.x - fi.x, dy = f.y - fi.y, dz = f.z - fi.z;
-                const bool pass = (HALF ? (j > i) : (j != i)) && (dx * dx + dy * dy + dz * dz < a.rs2_screen);
-                const unsigned msk = __ballot_sync(0xffffffffu, pass);
-                if (pass) myq[qn + __popc(msk & lt)] = s;
-                qn += __popc(msk);
-                if (qn >= 32) {
-                    __syncwarp();
-                    exact_flush(a, A, Gi, myq[lane], true, qi, L, halfL, dst, cap, cursor, lane);
-                    const int rest = lane < qn - 32 ? myq[32 + lane] : 0;
-                    __syncwarp();
-                    if (lane < qn - 32) myq[lane] = rest;
-                    qn -= 32;
+            int cursor = 0;
+            for (int k = lane; k < len32; k += 32) {
+                const int s = use_types ? (int)lst[k] : (k < M ? k : kMaxCand);
+                const int j = J[s];
+                const double2 xy = XY[s];
+                double dx = __dsub_rn(xy.x, qi.x), dy = __dsub_rn(xy.y, qi.y), dz = __dsub_rn(Z[s], qi.z);
+                const bool nx = image_needed(dx, half_hi), ny = image_needed(dy, half_hi), nz = image_needed(dz, half_hi);
+                if (__any_sync(0xffffffffu, nx | ny | nz)) {   // warp-uniform: rows near a box face only
+                    dx = image_apply(dx, L, nx);
+                    dy = image_apply(dy, L, ny);
+                    dz = image_apply(dz, L, nz);
                 }
+                const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                const bool acc = (HALF ? (j > i) : (j != i && j >= 0)) && __double_as_longlong(r2) < rs2_bits;
+                const unsigned msk = __ballot_sync(0xffffffffu, acc);
+                const int pos = cursor + __popc(msk & lt);
+                if (acc && pos < cap) dst[pos] = j;
+                cursor += __popc(msk);
             }
-            __syncwarp();
-            if (qn > 0) exact_flush(a, A, Gi, lane < qn ? myq[lane] : 0, lane < qn, qi, L, halfL, dst, cap, cursor,
-                                    lane);
-            __syncwarp();
             if (lane == 0 && !DIRECT) {
                 a.npart[r] = cursor;
                 if (cursor > kRowCap) atomicOr(&a.n_overflow[1], 1);
@@ -647,6 +718,7 @@ static ListArgs list_args(const CellGrid& cg, double rs, int half, int64_t row_b
     // widen the radius by 8e-7 L + 1e-5 so every exact pair passes the screen.
     double rsc = rs + 8e-7 * cg.L + 1e-5;
     a.rs2_screen = (float)(rsc * rsc);
+    a.r_screen = (float)(rsc * (1.0 + 1e-5));
     a.half = half;
     a.row_begin = row_begin;
     a.row_end = row_end;
@@ -663,7 +735,7 @@ static int list_grid(const CellGrid& cg, int per_sm) {
     return (int)(cg.ncell < g ? cg.ncell : g);
 }
 
-constexpr size_t kListSmem = (size_t)kMaxCand * 28 + kListWarps * 64 * sizeof(int);
+constexpr size_t kListSmem = (size_t)kMaxCand * 8 + (size_t)(kMaxCand + 32) * (3 * 8 + 4 + 1);
 
 cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
                               int32_t* npart, char* ws, const BuildWorkspace& W, cudaStream_t s) {
@@ -680,9 +752,9 @@ cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t r
     cudaError_t e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     if (half)
-        k_list_v2<0, 1><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+        k_list_v2<0, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
     else
-        k_list_v2<0, 0><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+        k_list_v2<0, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
     k_list_fallback<0><<<148, kListWarps * 32, 0, s>>>(a);
     g_launches += 2;
     return cudaGetLastError();
@@ -702,9 +774,9 @@ cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t r
     }
     ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, ptr, list, ws, W);
     if (half)
-        k_list_v2<1, 1><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+        k_list_v2<1, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
     else
-        k_list_v2<1, 0><<<list_grid(cg, 3), kListWarps * 32, kListSmem, s>>>(a);
+        k_list_v2<1, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
     k_list_fallback<1><<<148, kListWarps * 32, 0, s>>>(a);
     g_launches += 2;
     return cudaGetLastError();

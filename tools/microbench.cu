@@ -62,6 +62,71 @@ __global__ void k_gather(const rec4* __restrict__ q, int64_t rows, const int32_t
     if (s == 12345.678) out[0] = s;
 }
 
+
+// G=1 rows per thread, the CTA's CSR segment staged in shared memory first
+__global__ void k_gather_smem(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
+                              const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* out,
+                              int cap) {
+    extern __shared__ int sidx[];
+    const int64_t r0 = blockIdx.x * (int64_t)blockDim.x;
+    const int64_t r = r0 + threadIdx.x;
+    const int64_t rl = min(rows, r0 + (int64_t)blockDim.x);
+    const int64_t b = ptr[r0], e = ptr[rl];
+    const int64_t len = e - b;
+    double s = 0;
+    if (len <= cap) {
+        for (int64_t k = threadIdx.x; k < len; k += blockDim.x) sidx[k] = list[b + k];
+        __syncthreads();
+        if (r < rows) {
+            const int* l = sidx + (ptr[r] - b);
+            const int n = npart[r];
+            int k = 0;
+            for (; k + 4 <= n; k += 4) {
+                int j0 = l[k], j1 = l[k + 1], j2 = l[k + 2], j3 = l[k + 3];
+                rec4 a0 = ldrec(q + j0), a1 = ldrec(q + j1), a2 = ldrec(q + j2), a3 = ldrec(q + j3);
+                s += a0.x + a0.y + a0.z + a1.x + a1.y + a1.z + a2.x + a2.y + a2.z + a3.x + a3.y + a3.z;
+            }
+            for (; k < n; k++) {
+                rec4 a = ldrec(q + l[k]);
+                s += a.x + a.y + a.z;
+            }
+        }
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
+// G lanes per row, indices loaded 4 at a time (int4 from the 16-B aligned base)
+template <int G>
+__global__ void k_gather_vec(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
+                             const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* out) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t r = t / G;
+    int g = threadIdx.x % G;
+    double s = 0;
+    if (r < rows) {
+        const int64_t p0 = ptr[r];
+        const int n = npart[r];
+        const int64_t base = p0 & ~3ll;
+        const int off = (int)(p0 - base);
+        for (int c = 4 * g; c < off + n; c += 4 * G) {
+            int4 v = __ldg(reinterpret_cast<const int4*>(list + base + c));
+            int jj[4] = {v.x, v.y, v.z, v.w};
+            rec4 a[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                int k = c + u - off;
+                if (k >= 0 && k < n) a[u] = ldrec(q + jj[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                int k = c + u - off;
+                if (k >= 0 && k < n) s += a[u].x + a[u].y + a[u].z;
+            }
+        }
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
 __global__ void k_stream(const int4* __restrict__ a, int64_t n4, int* out) {
     int acc = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -90,6 +155,31 @@ int mb_gather(const double* q, int64_t rows, const int32_t* npart, const int64_t
         case 4: k_gather<4><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
         case 8: k_gather<8><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
         case 16: k_gather<16><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        default: return -1;
+    }
+    return (int)cudaGetLastError();
+}
+
+int mb_gather_smem(const double* q, int64_t rows, const int32_t* npart, const int64_t* ptr, const int32_t* list,
+                   double* out, int rows_per_cta, int cap, void* stream) {
+    unsigned grid = (unsigned)((rows + rows_per_cta - 1) / rows_per_cta);
+    cudaFuncSetAttribute(k_gather_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+    k_gather_smem<<<grid, rows_per_cta, cap * 4, (cudaStream_t)stream>>>((const rec4*)q, rows, npart, ptr, list, out,
+                                                                       cap);
+    return (int)cudaGetLastError();
+}
+
+int mb_gather_vec(const double* q, int64_t rows, const int32_t* npart, const int64_t* ptr, const int32_t* list,
+                  double* out, int G, void* stream) {
+    int64_t threads = rows * G;
+    unsigned grid = (unsigned)((threads + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    const rec4* qq = (const rec4*)q;
+    switch (G) {
+        case 1: k_gather_vec<1><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        case 2: k_gather_vec<2><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        case 4: k_gather_vec<4><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
+        case 8: k_gather_vec<8><<<grid, 256, 0, s>>>(qq, rows, npart, ptr, list, out); break;
         default: return -1;
     }
     return (int)cudaGetLastError();
