@@ -196,12 +196,12 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
-    if world > 1:
+    if world > 1 or "MASTER_ADDR" in os.environ:   # torchrun (any N): NCCL process group
         dist.init_process_group("nccl", device_id=dev)
         comm = dist.group.WORLD
 
     def barrier():
-        if world > 1:
+        if comm is not None:
             dist.barrier()
 
     w = lj_inputs.config(args.config)
@@ -263,7 +263,7 @@ def main():
     ck = clocks.stop()
     ms = t0.elapsed_time(t1)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if comm is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     entries_inside = sim.interactions()           # summed over ranks and timed steps
@@ -307,7 +307,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
+        if comm is not None:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e_pairs = sim.interactions()
         e_pairs = e_pairs if half else e_pairs / 2.0
@@ -347,7 +347,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if comm is not None:
         dist.destroy_process_group()
 
 

@@ -23,6 +23,7 @@ which has no fallback: it raises if liblj.so or the GPU is missing.
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import torch
 import torch.distributed as dist
@@ -96,6 +97,9 @@ class LeapfrogMD:
         self.be, self.g, self.dt = backend, g, float(dt)
         self.n = q_xyz.shape[0]
         self.rank, self.world, self.comm = rank, world, comm
+        # collectives run for P > 1; LJ_FORCE_COLLECTIVES=1 also issues them at P = 1 (exercises the
+        # NCCL code path on a single GPU under torchrun)
+        self.collective = comm is not None and (world > 1 or os.environ.get("LJ_FORCE_COLLECTIVES") == "1")
         self.rb, self.re = row_range(self.n, rank, world)
         self.q = backend.records(q_xyz)
         self.p = backend.records(p_xyz)
@@ -116,7 +120,7 @@ class LeapfrogMD:
     # ---- collectives (no-ops for one rank) ----
     def _allgather(self, x):
         """Replicate the own-row slab of x (n records) on every rank."""
-        if self.world > 1:
+        if self.collective:
             own = x[self.rb:self.re]
             if self.n % self.world == 0:
                 # in-place all-gather: rank r's slab is already at its offset
@@ -140,11 +144,11 @@ class LeapfrogMD:
         return dist.get_backend(self.comm) == "gloo"
 
     def _allreduce_max(self, t):
-        if self.world > 1:
+        if self.collective:
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.comm)
 
     def _allreduce_sum(self, t):
-        if self.world > 1:
+        if self.collective:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.comm)
 
     # ---- MD ----
@@ -156,7 +160,7 @@ class LeapfrogMD:
         """Wrap, (optionally) re-sort the atoms into cell order (§8(a) a3), snapshot
         q_ref and rebuild the own-row list (§8(a) a2-a4)."""
         if self.reorder:
-            if self.world > 1:
+            if self.collective:
                 self._allgather(self.p)          # momenta of all rows, to follow the permutation
             self.be.wrap(self.q, None)
             perm = self.be.cell_order(self.q)
