@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--order", default=None, choices=["lattice", "shuffled", "cell"],
                     help="storage order; default: config 2 shuffled, 3 cell, 4/5 cell (re-sorted at every rebuild)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--energy-every", type=int, default=None,
+                    help="NVE energy sample interval in timed steps (default: config 5 -> steps/20, else off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -217,31 +219,37 @@ def main():
     be = md.LibBackend(w.n, g, rb, re_, dev, half=half)
     sim = md.LeapfrogMD(be, w.q, w.p, g, w.dt, rank, world, comm, reorder=(order == "cell"))
     if not force_only:
-        sim.half_kick()   # leapfrog start: p_0 -> p_{1/2}
+        sim.start_leapfrog()   # p_0 -> p_{-1/2}
 
     stream = torch.cuda.current_stream()
     f_ev = []
 
-    def one_step(record):
-        if force_only:
-            if record:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-            be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
-            if record:
-                b.record(stream)
-                f_ev.append((a, b))
-            return
-        if record:
+    def one_step(record, sample=False):
+        """One step of the hot path; sample=True splits the kick around an energy
+        evaluation at synchronised momenta (config 5 NVE samples)."""
+        rec = record and not sample
+        if rec:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
-        if record:
+        e = None
+        if sample:
+            be.force(sim.q, sim.p, 0.5 * w.dt, sim.lst, sim.counter)
+            e = sim.energy()
+            be.force(sim.q, sim.p, 0.5 * w.dt, sim.lst)
+        else:
+            be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
+        if rec:
             b.record(stream)
             f_ev.append((a, b))
+        if force_only:
+            return e
         be.integrate(sim.q, sim.p, w.dt, sim.rb, sim.re)
         sim._allgather_q()
         sim.check_rebuild()
+        return e
+
+    every = args.energy_every if args.energy_every is not None else (max(1, args.steps // 20) if args.config == 5 else 0)
+    energies = []
 
     for _ in range(args.warmup):
         one_step(False)
@@ -254,8 +262,10 @@ def main():
     launches0 = lj.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for _ in range(args.steps):
-        one_step(True)
+    for k in range(args.steps):
+        e = one_step(True, sample=(every > 0 and not force_only and k % every == 0))
+        if e is not None:
+            energies.append((k, e[0], e[1]))
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -346,6 +356,15 @@ def main():
                                       "peak_gbs": pk.get("hbm_gbs"), "peak_kind": pk_kind}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         }
+        if energies:
+            E = np.array([ke + pe for _, ke, pe in energies])
+            ks = np.array([k for k, _, _ in energies], dtype=np.float64)
+            slope = float(np.polyfit(ks * w.dt, E / w.n, 1)[0]) if len(E) > 2 else None
+            line["nve"] = {"samples": len(E), "every": every, "E0_per_atom": float(E[0] / w.n),
+                           "drift_end_per_atom": float((E[-1] - E[0]) / w.n),
+                           "max_abs_dev_per_atom": float(np.abs(E - E[0]).max() / w.n),
+                           "slope_per_atom_per_time": slope, "note": "energy samples split the kick (KDK) at "
+                           "sample steps; their force time is excluded from ms_per_force_step"}
         print(json.dumps(line), flush=True)
     if comm is not None:
         dist.destroy_process_group()

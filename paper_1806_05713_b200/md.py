@@ -152,9 +152,13 @@ class LeapfrogMD:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.comm)
 
     # ---- MD ----
-    def half_kick(self):
-        """p += F(q) dt/2 -- turns p_0 into p_{1/2} (leapfrog start) or back."""
-        self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
+    def half_kick(self, sign: float = 1.0):
+        """p += sign F(q) dt/2."""
+        self.be.force(self.q, self.p, sign * 0.5 * self.dt, self.lst)
+
+    def start_leapfrog(self):
+        """Synchronised p_0 -> p_{-1/2} = p_0 - F(q_0) dt/2, the state step() expects."""
+        self.half_kick(-1.0)
 
     def _rebuild(self):
         """Wrap, (optionally) re-sort the atoms into cell order (§8(a) a3), snapshot
@@ -184,13 +188,23 @@ class LeapfrogMD:
             return True
         return False
 
-    def step(self):
-        """One leapfrog step: p += F(q) dt; q += p dt; all-gather; bookkeeping."""
-        self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
+    def step(self, sample: bool = False):
+        """One leapfrog step: p += F(q) dt; q += p dt; all-gather; bookkeeping.
+        With sample=True the kick is split in two halves around an energy
+        evaluation at the synchronised momenta p_n = p_{n-1/2} + F(q_n) dt/2
+        (reading O8/C-17); returns (KE, PE) then, else None."""
+        e = None
+        if sample:
+            self.be.force(self.q, self.p, 0.5 * self.dt, self.lst, self.counter)
+            e = self.energy()
+            self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
+        else:
+            self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
         self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
         self._allgather_q()
         self.check_rebuild()
         self.stats.steps += 1
+        return e
 
     def kdk_step(self):
         """One synchronised velocity-Verlet step (O8): kick dt/2, drift, rebuild check, kick dt/2."""

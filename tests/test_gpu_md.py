@@ -1,0 +1,59 @@
+"""GPU MD through the product driver (md.LeapfrogMD + liblj) against the oracle's
+NVE loop (reading O8; DESIGN.md Pin-10 on the GPU path)."""
+import numpy as np
+import pytest
+import torch
+
+import lj_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def md():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1806_05713_b200 import build, md as _md
+    build.build()
+    return _md
+
+
+@pytest.mark.parametrize("reorder", [True, False])
+def test_nve_matches_oracle(md, reorder):
+    from paper_1806_05713_b200 import lj
+    w = lj_inputs.make_system(10, jitter_seed=1, T=1.0, mom_seed=5, dt=0.005)
+    steps, every = 1000, 10
+    _, _, e_ref, rb_ref = oracle.md_run(w.q, w.p, w.L, w.rc, w.rs, w.dt, steps, every)
+    g = lj.geom(w.L, w.rc, w.rs)
+    dev = torch.device("cuda:0")
+    sim = md.LeapfrogMD(md.LibBackend(w.n, g, 0, w.n, dev), w.q, w.p, g, w.dt, reorder=reorder)
+    sim.start_leapfrog()
+    E = []
+    for k in range(steps + 1):
+        e = sim.step(sample=(k % every == 0))
+        if e is not None:
+            E.append(e[0] + e[1])
+    E = np.array(E)
+    Er = e_ref[:, 2]
+    assert len(E) == len(Er)
+    # identical start and, before chaos amplifies round-off, the same trajectory
+    assert E[0] == pytest.approx(Er[0], rel=1e-12)
+    assert np.allclose(E[:11], Er[:11], rtol=1e-9, atol=0)
+    # same fluctuation statistics over the whole run (Pin-10: ~1.05e-3 per atom)
+    fl, flr = np.abs(E - E[0]).max() / w.n, np.abs(Er - Er[0]).max() / w.n
+    assert 0.7 < fl / flr < 1.4
+    # the bookkeeping rebuild schedule is the oracle's (about every 9 steps)
+    assert abs(sim.stats.rebuilds - rb_ref) <= 3
+
+
+def test_momentum_conserved_over_md(md):
+    from paper_1806_05713_b200 import lj
+    w = lj_inputs.make_system(10, jitter_seed=3, T=1.0, mom_seed=8, dt=0.005)
+    g = lj.geom(w.L, w.rc, w.rs)
+    sim = md.LeapfrogMD(md.LibBackend(w.n, g, 0, w.n, torch.device("cuda:0")), w.q, w.p, g, w.dt)
+    sim.start_leapfrog()
+    for _ in range(200):
+        sim.step()
+    p = sim.p[:, :3].sum(dim=0).cpu().numpy()
+    assert np.all(np.abs(p) < 1e-10)
