@@ -85,6 +85,24 @@ lj_status lj_build_list(const double *q, int64_t n, lj_geom g, int half,
                         int32_t *sorted_list, int64_t capacity, int64_t *n_entries,
                         void *workspace, size_t workspace_bytes, void *stream);
 
+/* Layout flag of lj_build_list_ex: row r of the list starts at
+ * pointer[r] = r * LJ_PADDED_ROW_STRIDE (rows padded to a fixed stride; entries
+ * past number_of_partners[r] are undefined).  Saves the compaction pass of the
+ * compact CSR; every consumer of a list (force, energy) reads only
+ * [pointer[r], pointer[r] + number_of_partners[r]). */
+#define LJ_LIST_PADDED 1
+#define LJ_PADDED_ROW_STRIDE 192
+
+/* lj_build_list with layout flags (0 = compact CSR, as lj_build_list).  With
+ * LJ_LIST_PADDED, capacity must be >= rows * LJ_PADDED_ROW_STRIDE (else
+ * LJ_ERR_CAPACITY, *n_entries = that size); *n_entries receives the number of
+ * valid entries; a row longer than the stride returns LJ_ERR_UNSUPPORTED (use
+ * the compact layout).  Same synchronisation as lj_build_list. */
+lj_status lj_build_list_ex(const double *q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
+                           int flags, int32_t *number_of_partners, int64_t *pointer, int32_t *sorted_list,
+                           int64_t capacity, int64_t *n_entries, void *workspace, size_t workspace_bytes,
+                           void *stream);
+
 /* Spatial reordering (BASELINE.json config 3): perm[new] = old, the stable
  * sort of the atoms by cell id (cx*nc + cy)*nc + cz (same cells as the list). */
 lj_status lj_cell_order(const double *q, int64_t n, lj_geom g, int64_t *perm,

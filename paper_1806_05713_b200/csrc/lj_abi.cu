@@ -125,12 +125,14 @@ lj_status lj_build_list_workspace(int64_t n, lj_geom g, size_t* bytes) {
     return LJ_OK;
 }
 
-lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
-                        int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list, int64_t capacity,
-                        int64_t* n_entries, void* workspace, size_t workspace_bytes, void* stream) {
+lj_status lj_build_list_ex(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
+                           int flags, int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list,
+                           int64_t capacity, int64_t* n_entries, void* workspace, size_t workspace_bytes,
+                           void* stream) {
     LJ_TRY(check_n(n));
     LJ_TRY(check_geom(g, true));
     LJ_TRY(check_rows(n, row_begin, row_end));
+    if (flags & ~LJ_LIST_PADDED) return fail(LJ_ERR_ARG, "build_list: unknown flags 0x%x", flags);
     if (half && (row_begin != 0 || row_end != n))
         return fail(LJ_ERR_UNSUPPORTED, "half list must cover all rows [0,n) (SURVEY §8(e))");
     if (!n_entries || !pointer || (row_end > row_begin && !number_of_partners) || (n > 0 && !q))
@@ -145,15 +147,23 @@ lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)workspace;
     const int64_t rows = row_end - row_begin;
+    const bool padded = (flags & LJ_LIST_PADDED) != 0;
+    if (padded && capacity < rows * (int64_t)LJ_PADDED_ROW_STRIDE) {
+        *n_entries = rows * (int64_t)LJ_PADDED_ROW_STRIDE;
+        return fail(LJ_ERR_CAPACITY, "build_list: padded layout needs capacity %lld", (long long)*n_entries);
+    }
+    int64_t* counts_scan = padded ? (int64_t*)(ws + W.off_ptrtmp) : pointer;
     LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
     if (rows > 0)
-        LJ_CUDA(launch_list_pass1(cg, g.rs, half, row_begin, row_end, number_of_partners, ws, W, s),
+        LJ_CUDA(launch_list_pass1(cg, g.rs, half, row_begin, row_end, number_of_partners,
+                                  padded ? sorted_list : nullptr, ws, W, s),
                 "lj_build_list/pass1");
-    LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, pointer, rows, (int64_t*)(ws + W.off_scan), W.scan_blocks, s),
+    LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, counts_scan, rows, (int64_t*)(ws + W.off_scan),
+                                   W.scan_blocks, s),
             "lj_build_list/scan");
     int64_t total = 0;
     int32_t row_overflow = 0;
-    LJ_CUDA(cudaMemcpyAsync(&total, pointer + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+    LJ_CUDA(cudaMemcpyAsync(&total, counts_scan + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
             "lj_build_list/readback");
     if (rows > 0)
         LJ_CUDA(cudaMemcpyAsync(&row_overflow, list_row_overflow_flag(ws, W), sizeof(int32_t), cudaMemcpyDeviceToHost,
@@ -161,6 +171,13 @@ lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t
                 "lj_build_list/readback");
     LJ_CUDA(cudaStreamSynchronize(s), "lj_build_list/sync");
     *n_entries = total;
+    if (padded) {
+        if (row_overflow)
+            return fail(LJ_ERR_UNSUPPORTED, "build_list: a row has more than %d partners; use the compact layout",
+                        LJ_PADDED_ROW_STRIDE);
+        LJ_CUDA(launch_padded_pointer(pointer, rows, s), "lj_build_list/pointer");
+        return LJ_OK;
+    }
     if (total > capacity)
         return fail(LJ_ERR_CAPACITY, "build_list: capacity %lld < required %lld", (long long)capacity,
                     (long long)total);
@@ -169,6 +186,13 @@ lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t
                                   row_overflow != 0, ws, W, s),
                 "lj_build_list/pass2");
     return LJ_OK;
+}
+
+lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
+                        int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list, int64_t capacity,
+                        int64_t* n_entries, void* workspace, size_t workspace_bytes, void* stream) {
+    return lj_build_list_ex(q, n, g, half, row_begin, row_end, 0, number_of_partners, pointer, sorted_list, capacity,
+                            n_entries, workspace, workspace_bytes, stream);
 }
 
 lj_status lj_cell_order(const double* q, int64_t n, lj_geom g, int64_t* perm, void* workspace,

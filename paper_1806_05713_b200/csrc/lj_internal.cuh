@@ -39,7 +39,7 @@ struct CellGrid {
 // Workspace carve-out (offsets in bytes, 256-B aligned).
 struct BuildWorkspace {
     size_t off_cell_of, off_count, off_start, off_cursor, off_atoms, off_qcell, off_qf, off_scan, off_over,
-        off_scratch, total;
+        off_ptrtmp, off_scratch, total;
     int64_t scan_blocks;
 };
 
@@ -49,8 +49,10 @@ BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows);
 cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* ws, const BuildWorkspace& W,
                          cudaStream_t s);
 // pass 1: every row into the per-row scratch (stride kRowCap), counts into npart
+// (out == nullptr: the workspace scratch; else the caller's padded list)
 cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
-                              int32_t* npart, char* ws, const BuildWorkspace& W, cudaStream_t s);
+                              int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W, cudaStream_t s);
+cudaError_t launch_padded_pointer(int64_t* ptr, int64_t rows, cudaStream_t s);
 // pass 2: scratch -> CSR, or (if some row overflowed the scratch) a direct fill at pointer[r]
 cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
                               int32_t* npart, const int64_t* ptr, int32_t* list, bool row_overflow, char* ws,

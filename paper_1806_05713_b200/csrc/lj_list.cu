@@ -659,6 +659,8 @@ BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows) {
     o = align256(o + sizeof(int64_t) * (size_t)(W.scan_blocks + 1));
     W.off_over = o;    // [0] overflow cell count, [1] row overflow flag, then ncell cell ids
     o = align256(o + sizeof(int32_t) * (size_t)(ncell + 2));
+    W.off_ptrtmp = o;  // rows + 1 int64 (padded layout: scan of the counts)
+    o = align256(o + sizeof(int64_t) * (size_t)(rows + 1));
     W.off_scratch = o; // rows * kRowCap int32
     o = align256(o + sizeof(int32_t) * (size_t)rows * kRowCap);
     W.total = o;
@@ -738,7 +740,7 @@ static int list_grid(const CellGrid& cg, int per_sm) {
 constexpr size_t kListSmem = (size_t)kMaxCand * 8 + (size_t)(kMaxCand + 32) * (3 * 8 + 4 + 1);
 
 cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
-                              int32_t* npart, char* ws, const BuildWorkspace& W, cudaStream_t s) {
+                              int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         void (*fns[4])(ListArgs) = {k_list_v2<0, 0>, k_list_v2<0, 1>, k_list_v2<1, 0>, k_list_v2<1, 1>};
@@ -748,7 +750,8 @@ cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t r
         }
         attr = true;
     }
-    ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, nullptr, (int32_t*)(ws + W.off_scratch), ws, W);
+    ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, nullptr,
+                           out ? out : (int32_t*)(ws + W.off_scratch), ws, W);
     cudaError_t e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     if (half)
@@ -779,6 +782,17 @@ cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t r
         k_list_v2<1, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
     k_list_fallback<1><<<148, kListWarps * 32, 0, s>>>(a);
     g_launches += 2;
+    return cudaGetLastError();
+}
+
+__global__ void k_padded_pointer(int64_t* ptr, int64_t rows) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= rows; r += (int64_t)gridDim.x * blockDim.x)
+        ptr[r] = r * (int64_t)kRowCap;
+}
+
+cudaError_t launch_padded_pointer(int64_t* ptr, int64_t rows, cudaStream_t s) {
+    k_padded_pointer<<<grid_for(rows + 1, 256), 256, 0, s>>>(ptr, rows);
+    g_launches++;
     return cudaGetLastError();
 }
 

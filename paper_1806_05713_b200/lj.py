@@ -17,10 +17,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblj.so")
 
 LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 192   # include/liblj.h
 
 # every symbol include/liblj.h declares
 EXPORTS = (
-    "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_cell_order",
+    "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_cell_order",
     "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_integrate", "lj_wrap",
     "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
     "lj_version",
@@ -59,6 +60,8 @@ def load() -> ctypes.CDLL:
         "lj_unpack_aos4": (st, [vp, vp, i64, vp]),
         "lj_build_list_workspace": (st, [i64, Geom, ctypes.POINTER(sz)]),
         "lj_build_list": (st, [vp, i64, Geom, i32, i64, i64, vp, vp, vp, i64, ctypes.POINTER(i64), vp, sz, vp]),
+        "lj_build_list_ex": (st, [vp, i64, Geom, i32, i64, i64, i32, vp, vp, vp, i64, ctypes.POINTER(i64), vp, sz,
+                                  vp]),
         "lj_cell_order": (st, [vp, i64, Geom, vp, vp, sz, vp]),
         "lj_permute_rows": (st, [vp, vp, vp, i64, vp]),
         "lj_force_step": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, vp]),
@@ -155,7 +158,7 @@ class ListBuilder:
     """Holds the build workspace and a growing list buffer for repeated rebuilds."""
 
     def __init__(self, n: int, g: Geom, half: bool, row_begin: int = 0, row_end: int | None = None,
-                 device=None, headroom: float = 1.15, initial_per_row: int = 0):
+                 device=None, headroom: float = 1.15, initial_per_row: int = 0, padded: bool = False):
         self.n, self.g, self.half = int(n), g, bool(half)
         self.row_begin = int(row_begin)
         self.row_end = int(n if row_end is None else row_end)
@@ -167,6 +170,9 @@ class ListBuilder:
         rows = self.row_end - self.row_begin
         self.npart = torch.empty(max(rows, 1), dtype=torch.int32, device=self.device)
         self.pointer = torch.empty(rows + 1, dtype=torch.int64, device=self.device)
+        self.padded = padded
+        if padded:
+            initial_per_row = LJ_PADDED_ROW_STRIDE
         self.sorted_list = torch.empty(max(int(rows * initial_per_row), 1), dtype=torch.int32, device=self.device)
         self.rebuilds = 0
 
@@ -174,11 +180,15 @@ class ListBuilder:
         _rec(q, "q")
         L = load()
         ne = ctypes.c_int64(0)
-        for _ in range(2):
-            st = L.lj_build_list(_ptr(q), self.n, self.g, int(self.half), self.row_begin, self.row_end,
-                                 _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
-                                 self.sorted_list.numel(), ctypes.byref(ne), _ptr(self.workspace),
-                                 self.workspace.numel(), _stream())
+        for _ in range(3):
+            st = L.lj_build_list_ex(_ptr(q), self.n, self.g, int(self.half), self.row_begin, self.row_end,
+                                    LJ_LIST_PADDED if self.padded else 0,
+                                    _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
+                                    self.sorted_list.numel(), ctypes.byref(ne), _ptr(self.workspace),
+                                    self.workspace.numel(), _stream())
+            if st == LJ_ERR_UNSUPPORTED and self.padded:   # a row longer than the stride: compact from now on
+                self.padded = False
+                continue
             if st == LJ_ERR_CAPACITY:
                 cap = int(ne.value * self.headroom) + 1024
                 self.sorted_list = torch.empty(cap, dtype=torch.int32, device=self.device)

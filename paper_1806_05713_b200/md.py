@@ -43,7 +43,7 @@ class LibBackend:
         lj.load()
         self.device = torch.device(device)
         self.n, self.g = n, g
-        self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device)
+        self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device, padded=True)
 
     def records(self, xyz):
         t = xyz if isinstance(xyz, torch.Tensor) else torch.from_numpy(xyz)

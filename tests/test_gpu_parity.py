@@ -343,3 +343,44 @@ def test_kdk_step_matches_oracle(lj, dev):
     assert oracle.parity_error(from_dev(p), p1, S) <= TOL
     # positions differ only through p_{1/2} rounding: tiny absolute error
     assert np.abs(from_dev(q) - q1).max() < 1e-14
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+@pytest.mark.parametrize("half", [True, False])
+def test_padded_layout_same_rows(lj, dev, systems, cfg, half):
+    """LJ_LIST_PADDED: pointer[r] = r * stride, rows identical to the oracle's."""
+    w = systems[cfg]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    b = lj.ListBuilder(w.n, g, half, device=dev, padded=True)
+    gl = b.build(q)
+    assert b.padded
+    ol = oracle.list_cells(w.q, w.L, w.rs, half)
+    assert gl.n_entries == ol.n_entries
+    ptr = gl.pointer.cpu().numpy()
+    assert np.array_equal(ptr, np.arange(w.n + 1) * lj.LJ_PADDED_ROW_STRIDE)
+    npart = gl.number_of_partners.cpu().numpy()
+    assert np.array_equal(npart, ol.number_of_partners)
+    sl = gl.sorted_list.cpu().numpy()
+    for r in range(0, w.n, 97):
+        assert np.array_equal(sl[ptr[r]:ptr[r] + npart[r]], ol.row(r))
+    # force over the padded list = force over the compact list (same summation order per row)
+    p0 = np.random.default_rng(1).normal(0, 1, (w.n, 3))
+    pa, pb = to_dev(p0, dev), to_dev(p0, dev)
+    lj.force_step(q, pa, g, w.dt, gl)
+    lj.force_step(q, pb, g, w.dt, lj.build_list(q, g, half))
+    if half:
+        ref, S, _ = oracle_force(w, p0, True)
+        assert oracle.parity_error(from_dev(pa), ref, S) <= TOL
+    else:
+        assert torch.equal(pa, pb)
+
+
+def test_padded_layout_falls_back_on_long_rows(lj, dev):
+    """Rows longer than the stride (dense gas) -> UNSUPPORTED -> the builder switches to compact."""
+    q = lj_inputs.random_gas(5000, 9.9, 4)
+    g = lj.geom(9.9, 3.0, 3.3)
+    b = lj.ListBuilder(5000, g, False, device=dev, padded=True)
+    gl = b.build(to_dev(q, dev))
+    assert not b.padded
+    assert_same_list(gl, oracle.list_cells(q, 9.9, 3.3, False))
