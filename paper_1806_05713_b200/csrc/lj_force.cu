@@ -116,14 +116,24 @@ __global__ void __launch_bounds__(kForceThreads)
         const rec4 qi = load_rec(q, i);
         const int32_t* __restrict__ lst = list + ptr[r];
         const int n = npart[r];
+        // software pipeline (the GPU analogue of the paper's SWP): the
+        // indices of chunk k+1 are loaded before the records of chunk k are used
+        int jn[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
         for (int k0 = g; k0 < n; k0 += U * G) {
             int j[U];
             rec4 qj[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) j[u] = (k0 + u * G < n) ? __ldg(lst + k0 + u * G) : -1;
+            for (int u = 0; u < U; u++) j[u] = jn[u];
 #pragma unroll
             for (int u = 0; u < U; u++)
                 if (j[u] >= 0) qj[u] = load_rec(q, j[u]);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int kn = k0 + U * G + u * G;
+                jn[u] = kn < n ? __ldg(lst + kn) : -1;
+            }
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 if (j[u] >= 0) {
