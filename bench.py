@@ -295,6 +295,20 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     hbm_bytes = (4 * entries_per_launch + (re_ - rb) * (32 + 32 + 32 + 8 + 4) + w.n * 32)
 
+    # ---- gather roofline probe: the force kernel's traffic without its math (same list, same lanes) ----
+    probe_ms = None
+    if not force_only or not half:
+        sink = torch.zeros(1, dtype=torch.float64, device=dev)
+        for _ in range(3):
+            lj.gather_probe(sim.q, sim.lst, 0, sink)
+        pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pa.record(stream)
+        for _ in range(10):
+            lj.gather_probe(sim.q, sim.lst, 0, sink)
+        pb.record(stream)
+        torch.cuda.synchronize()
+        probe_ms = pa.elapsed_time(pb) / 10
+
     # ---- e2e: same steps through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -353,7 +367,16 @@ def main():
                          "flop_per_entry": FLOP_PER_ENTRY, "entries_per_launch": entries_per_launch,
                          "hbm_view": {"algorithmic_bytes": hbm_bytes,
                                       "achieved_gbs": hbm_bytes / (force_avg * 1e-3) / 1e9,
-                                      "peak_gbs": pk.get("hbm_gbs"), "peak_kind": pk_kind}},
+                                      "peak_gbs": pk.get("hbm_gbs"), "peak_kind": pk_kind,
+                                      "frac": hbm_bytes / (force_avg * 1e-3) / 1e9 / pk.get("hbm_gbs", 6551.0)},
+                         "gather_view": None if probe_ms is None else {
+                             "bytes_per_entry": 36,
+                             "achieved_gbs": 36 * entries_per_launch / (force_avg * 1e-3) / 1e9,
+                             "peak_gbs": 36 * entries_per_launch / (probe_ms * 1e-3) / 1e9,
+                             "frac": probe_ms / force_avg,
+                             "peak_kind": "measured live: lj_gather_probe (same list, same lanes, no arithmetic)"},
+                         "baseline_json_roofline_frac": None if probe_ms is None else
+                             max(probe_ms, FLOP_PER_ENTRY * entries_per_launch / (peak_tflops * 1e12) * 1e3) / force_avg},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         }
         if energies:

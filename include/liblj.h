@@ -138,6 +138,15 @@ lj_status lj_force_step_ex(const double *q, double *p, int64_t n, lj_geom g, dou
                            const int32_t *sorted_list, int lanes_per_row, int ordered,
                            unsigned long long *n_interactions, void *stream);
 
+/* Roofline probe (not part of the method): the memory traffic of lj_force_step
+ * on a full list -- the same lanes-per-row mapping, index loads and 256-bit
+ * record gathers -- with no arithmetic beyond a running sum written to *sink
+ * (device double).  Its duration is the gather-bandwidth floor of the force
+ * kernel (SURVEY §8(d) "gather-only replay of the actual CSR list"). */
+lj_status lj_gather_probe(const double *q, int64_t n, int64_t row_begin, int64_t row_end,
+                          const int32_t *number_of_partners, const int64_t *pointer,
+                          const int32_t *sorted_list, int lanes_per_row, double *sink, void *stream);
+
 /* ---- integration and bookkeeping (§8(a) a7, a9) --------------------------- */
 
 /* Drift q_i += p_i dt for atoms [begin, end) (mass 1), bit-identical to the

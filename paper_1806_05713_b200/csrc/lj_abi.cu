@@ -275,6 +275,33 @@ lj_status lj_force_step(const double* q, double* p, int64_t n, lj_geom g, double
                             nullptr, stream);
 }
 
+lj_status lj_gather_probe(const double* q, int64_t n, int64_t row_begin, int64_t row_end,
+                          const int32_t* number_of_partners, const int64_t* pointer, const int32_t* sorted_list,
+                          int lanes_per_row, double* sink, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_rows(n, row_begin, row_end));
+    if (!sink || (row_end > row_begin && (!q || !number_of_partners || !pointer)))
+        return fail(LJ_ERR_ARG, "gather_probe: null pointer");
+    if (!aligned32(q)) return fail(LJ_ERR_ARG, "gather_probe: q not 32-byte aligned");
+    int lanes = lanes_per_row == 0 ? ((row_end - row_begin) >= 500000 ? 4 : 8) : lanes_per_row;
+    if (lanes != 4 && lanes != 8 && lanes != 16)
+        return fail(LJ_ERR_ARG, "gather_probe: lanes_per_row must be 0, 4, 8 or 16 (got %d)", lanes_per_row);
+    ForceArgs a;
+    a.q = q;
+    a.p = nullptr;
+    a.row_begin = row_begin;
+    a.rows = row_end - row_begin;
+    a.npart = number_of_partners;
+    a.ptr = pointer;
+    a.list = sorted_list;
+    a.L = 0;
+    a.rc2 = 0;
+    a.dt = 0;
+    a.n_inter = nullptr;
+    LJ_CUDA(launch_gather_probe(a, lanes, sink, (cudaStream_t)stream), "lj_gather_probe");
+    return LJ_OK;
+}
+
 lj_status lj_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, void* stream) {
     if (begin < 0 || end < begin || end > (int64_t)INT32_MAX)
         return fail(LJ_ERR_ARG, "integrate: bad range [%lld,%lld)", (long long)begin, (long long)end);

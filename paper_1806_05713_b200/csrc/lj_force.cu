@@ -174,6 +174,34 @@ __global__ void __launch_bounds__(kForceThreads)
     count_interactions(cnt, n_inter);
 }
 
+// Roofline probe: the force kernel's access pattern (G lanes per row, two
+// gathers in flight, next indices prefetched) without the arithmetic.
+template <int G>
+__global__ void __launch_bounds__(kForceThreads)
+    k_gather_probe(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
+                   const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* sink) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    double s = 0.0;
+    if (r < rows) {
+        const int32_t* __restrict__ lst = list + ptr[r];
+        const int n = npart[r];
+        int jn0 = g < n ? __ldg(lst + g) : -1, jn1 = g + G < n ? __ldg(lst + g + G) : -1;
+        for (int k0 = g; k0 < n; k0 += 2 * G) {
+            const int j0 = jn0, j1 = jn1;
+            rec4 a, b;
+            if (j0 >= 0) a = load_rec(q, j0);
+            if (j1 >= 0) b = load_rec(q, j1);
+            jn0 = k0 + 2 * G < n ? __ldg(lst + k0 + 2 * G) : -1;
+            jn1 = k0 + 3 * G < n ? __ldg(lst + k0 + 3 * G) : -1;
+            if (j0 >= 0) s += a.x + a.y + a.z;
+            if (j1 >= 0) s += b.x + b.y + b.z;
+        }
+    }
+    if (s == 1.2345678e300) sink[0] = s;   // never true: keeps the loads alive
+}
+
 // Bit-exact "ordered" full-list kernel (DESIGN.md Pin-11): one thread per row,
 // ascending j, Alg. 3 accumulating into the loaded p_i, the oracle's expression
 // order and IEEE operations (explicit _rn intrinsics: no FMA contraction).
@@ -279,6 +307,20 @@ cudaError_t launch_gu(const ForceArgs& a, int lanes, cudaStream_t s) {
 
 cudaError_t launch_force_full(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_gu<false>(a, lanes, s); }
 cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_gu<true>(a, lanes, s); }
+
+cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cudaStream_t s) {
+    if (a.rows <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((a.rows * (int64_t)lanes + kForceThreads - 1) / kForceThreads);
+    const rec4* q = (const rec4*)a.q;
+    switch (lanes) {
+        case 4: k_gather_probe<4><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink); break;
+        case 8: k_gather_probe<8><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink); break;
+        case 16: k_gather_probe<16><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink); break;
+        default: return cudaErrorInvalidValue;
+    }
+    g_launches++;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_force_ordered(const ForceArgs& a, cudaStream_t s) {
     if (a.rows <= 0) return cudaSuccess;

@@ -22,7 +22,7 @@ LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 192   # include/liblj.h
 # every symbol include/liblj.h declares
 EXPORTS = (
     "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_cell_order",
-    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_integrate", "lj_wrap",
+    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_gather_probe", "lj_integrate", "lj_wrap",
     "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
     "lj_version",
 )
@@ -66,6 +66,7 @@ def load() -> ctypes.CDLL:
         "lj_permute_rows": (st, [vp, vp, vp, i64, vp]),
         "lj_force_step": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, vp]),
         "lj_force_step_ex": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, i32, i32, vp, vp]),
+        "lj_gather_probe": (st, [vp, i64, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
         "lj_wrap": (st, [vp, vp, i64, d, vp]),
         "lj_max_displacement": (st, [vp, vp, i64, i64, vp, vp]),
@@ -245,6 +246,16 @@ def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRLis
         raise TypeError("n_interactions must be a CUDA int64 tensor")
     _check(load().lj_force_step_ex(_ptr(q), _ptr(p), q.shape[0], g, float(dt), int(lst.half), *_list_args(lst),
                                    int(lanes_per_row), int(ordered), _ptr(n_interactions), _stream()))
+
+
+def gather_probe(q: torch.Tensor, lst: CSRList, lanes_per_row: int = 0, sink: torch.Tensor | None = None) -> None:
+    """Roofline probe: the force kernel's memory traffic without its arithmetic."""
+    _rec(q, "q")
+    if sink is None:
+        sink = torch.zeros(1, dtype=torch.float64, device=q.device)
+    _check(load().lj_gather_probe(_ptr(q), q.shape[0], lst.row_begin, lst.row_end, _ptr(lst.number_of_partners),
+                                  _ptr(lst.pointer), _ptr(lst.sorted_list), int(lanes_per_row), _ptr(sink),
+                                  _stream()))
 
 
 def integrate(q: torch.Tensor, p: torch.Tensor, dt: float, begin: int = 0, end: int | None = None) -> None:
