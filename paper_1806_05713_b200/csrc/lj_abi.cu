@@ -155,7 +155,7 @@ lj_status lj_build_list_ex(const double* q, int64_t n, lj_geom g, int half, int6
     int64_t* counts_scan = padded ? (int64_t*)(ws + W.off_ptrtmp) : pointer;
     LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
     if (rows > 0)
-        LJ_CUDA(launch_list_pass1(cg, g.rs, half, row_begin, row_end, number_of_partners,
+        LJ_CUDA(launch_list_pass1(q, cg, g.rs, half, row_begin, row_end, number_of_partners,
                                   padded ? sorted_list : nullptr, ws, W, s),
                 "lj_build_list/pass1");
     LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, counts_scan, rows, (int64_t*)(ws + W.off_scan),
@@ -182,7 +182,7 @@ lj_status lj_build_list_ex(const double* q, int64_t n, lj_geom g, int half, int6
         return fail(LJ_ERR_CAPACITY, "build_list: capacity %lld < required %lld", (long long)capacity,
                     (long long)total);
     if (rows > 0 && total > 0)
-        LJ_CUDA(launch_list_pass2(cg, g.rs, half, row_begin, row_end, number_of_partners, pointer, sorted_list,
+        LJ_CUDA(launch_list_pass2(q, cg, g.rs, half, row_begin, row_end, number_of_partners, pointer, sorted_list,
                                   row_overflow != 0, ws, W, s),
                 "lj_build_list/pass2");
     return LJ_OK;

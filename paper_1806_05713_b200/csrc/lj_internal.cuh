@@ -38,8 +38,8 @@ struct CellGrid {
 
 // Workspace carve-out (offsets in bytes, 256-B aligned).
 struct BuildWorkspace {
-    size_t off_cell_of, off_count, off_start, off_cursor, off_atoms, off_qcell, off_qf, off_scan, off_over,
-        off_ptrtmp, off_scratch, total;
+    size_t off_cell_of, off_count, off_start, off_cursor, off_atoms, off_qcell, off_qf, off_qr, off_scan, off_over,
+        off_flags, off_ptrtmp, off_scratch, total;
     int64_t scan_blocks;
 };
 
@@ -50,13 +50,14 @@ cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* w
                          cudaStream_t s);
 // pass 1: every row into the per-row scratch (stride kRowCap), counts into npart
 // (out == nullptr: the workspace scratch; else the caller's padded list)
-cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
-                              int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W, cudaStream_t s);
+cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
+                              int64_t row_end, int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W,
+                              cudaStream_t s);
 cudaError_t launch_padded_pointer(int64_t* ptr, int64_t rows, cudaStream_t s);
 // pass 2: scratch -> CSR, or (if some row overflowed the scratch) a direct fill at pointer[r]
-cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
-                              int32_t* npart, const int64_t* ptr, int32_t* list, bool row_overflow, char* ws,
-                              const BuildWorkspace& W, cudaStream_t s);
+cudaError_t launch_list_pass2(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
+                              int64_t row_end, int32_t* npart, const int64_t* ptr, int32_t* list, bool row_overflow,
+                              char* ws, const BuildWorkspace& W, cudaStream_t s);
 const int32_t* list_row_overflow_flag(char* ws, const BuildWorkspace& W);
 // exclusive scan of int32 counts -> int64 offsets (out has n+1 entries)
 cudaError_t launch_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, int64_t* block_sums,

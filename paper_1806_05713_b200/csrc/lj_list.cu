@@ -18,6 +18,7 @@
 //   same branches, r2 = (dx*dx + dy*dy) + dz*dz with explicit _rn intrinsics
 //   (no FMA contraction), strict r2 < rs2 with rs2 = rs*rs computed on the host.
 #include <climits>
+#include <cmath>
 
 #include "lj_internal.cuh"
 
@@ -95,14 +96,22 @@ __device__ __forceinline__ int next_pow2(int x) {
 
 // ---- cells ---------------------------------------------------------------
 
+// Also raises flags[0] if some raw coordinate lies outside [0, L): the fast
+// list kernel (k_list_v4) needs wrapped input, the exact kernel handles the rest.
 __global__ void k_cell_assign(const rec4* __restrict__ q, int64_t n, CellGrid cg, int32_t* __restrict__ cell_of,
-                              int32_t* __restrict__ count) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        rec4 r = q[i];
-        int cx = cell_coord(r.x, cg), cy = cell_coord(r.y, cg), cz = cell_coord(r.z, cg);
-        int c = (cx * cg.nc + cy) * cg.nc + cz;
-        cell_of[i] = c;
-        atomicAdd(&count[c], 1);
+                              int32_t* __restrict__ count, int32_t* __restrict__ flags) {
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        bool outside = false;
+        if (i < n) {
+            rec4 r = q[i];
+            int cx = cell_coord(r.x, cg), cy = cell_coord(r.y, cg), cz = cell_coord(r.z, cg);
+            int c = (cx * cg.nc + cy) * cg.nc + cz;
+            cell_of[i] = c;
+            atomicAdd(&count[c], 1);
+            outside = !(r.x >= 0.0 && r.x < cg.L && r.y >= 0.0 && r.y < cg.L && r.z >= 0.0 && r.z < cg.L);
+        }
+        if (__any_sync(0xffffffffu, outside) && (threadIdx.x & 31) == 0) atomicOr(&flags[0], 1);
     }
 }
 
@@ -124,7 +133,7 @@ __device__ __forceinline__ double wrap_exact(double x, double L) {
 
 __global__ void k_cell_sort_gather(const rec4* __restrict__ q, CellGrid cg, const int64_t* __restrict__ start,
                                    int32_t* __restrict__ atoms, rec4* __restrict__ q_cell,
-                                   float4* __restrict__ qf_cell) {
+                                   float4* __restrict__ qf_cell, float4* __restrict__ qr_cell, double cw) {
     const int64_t ncell = cg.ncell;
     __shared__ int buf[kListWarps][kCellBuf];
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -149,11 +158,16 @@ __global__ void k_cell_sort_gather(const rec4* __restrict__ q, CellGrid cg, cons
             }
         }
         __syncwarp();
+        const int cz = (int)(c % cg.nc), cy = (int)((c / cg.nc) % cg.nc), cx = (int)(c / ((int64_t)cg.nc * cg.nc));
+        const double ox = cx * cw, oy = cy * cw, oz = cz * cw;
         for (int k = lane; k < cnt; k += 32) {
-            const rec4 r = q[atoms[s + k]];
+            const int i = atoms[s + k];
+            const rec4 r = q[i];
             q_cell[s + k] = r;
             qf_cell[s + k] = make_float4((float)wrap_exact(r.x, cg.L), (float)wrap_exact(r.y, cg.L),
                                          (float)wrap_exact(r.z, cg.L), 0.0f);
+            // fp32 coordinates relative to the cell's corner + atom index (k_list_v4 staging)
+            qr_cell[s + k] = make_float4((float)(r.x - ox), (float)(r.y - oy), (float)(r.z - oz), __int_as_float(i));
         }
     }
 }
@@ -188,6 +202,7 @@ __device__ __forceinline__ int neighbour_cell(int c, int t, const CellGrid& cg, 
 struct ListArgs {
     const rec4* q_cell;       // positions in cell order (raw, for the exact test)
     const float4* qf_cell;    // wrapped positions in cell order, fp32 (screen only)
+    const float4* qr_cell;    // fp32 coordinates relative to the own cell's corner + atom index (v4)
     const int32_t* atoms;     // cell order -> atom index
     const int64_t* start;     // cell -> first slot (ncell + 1)
     int64_t ncell;
@@ -202,6 +217,12 @@ struct ListArgs {
     int32_t* out;             // scratch [rows * kRowCap] or list
     int32_t* overflow_cells;  // cells with more than kMaxCand candidates
     int32_t* n_overflow;      // [0] = #overflow cells, [1] = row overflow flag
+    // v4 (fast path, wrapped input only)
+    const rec4* q;            // raw input positions (atom order): the exact band test
+    const int32_t* flags;     // [0] != 0: some coordinate outside [0, L) -> exact kernel instead
+    double w;                 // cell width L / nc
+    float lo2, hi2;           // fp32 decision band around rs2: r2f < lo2 accept, r2f >= hi2 reject
+    float rb2;                // squared reach of a half-cell box (rounded-box candidate screen)
 };
 
 // Exact accept test on raw fp64 coordinates, bit-identical to the oracle's
@@ -230,6 +251,7 @@ __device__ __forceinline__ double image_apply(double d, double L, bool need) {
 // therefore comes out ascending.  No global loads in the inner loop.
 template <int DIRECT, int HALF>
 __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
+    if (!a.flags[0]) return;   // wrapped input: k_list_v4 builds the list
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);   // staging keys, then type lists
     unsigned short* tl = reinterpret_cast<unsigned short*>(smem);
@@ -459,6 +481,328 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
     }
 }
 
+// Builder v4 (fast path; every raw coordinate in [0, L), i.e. wrapped input as
+// the MD driver and the generators provide -- else k_list_v2 runs instead).
+//
+// Same cell/stencil decomposition as v3, but:
+//  * candidates are staged as fp32 coordinates relative to the cell's corner:
+//    u = (x - own corner) [precomputed per atom by k_cell_sort_gather] + the
+//    neighbour cell's offset (-w, 0 or w per axis), plus the atom index;
+//  * a half-cell's candidate list holds the candidates within the squared reach
+//    rb2 of the half-cell BOX (rounded-box screen: ~382 of ~1000 candidates
+//    at rho = 1, r_s = 3.3, instead of the ~570 of the v3 reach cube); warp tau
+//    builds the list of type tau in one ordered pass (ballot compaction);
+//  * loops swapped: a work item is (half-cell type, <= kItemRows rows of that
+//    type); the rows live in registers, each lane holds two candidates of a
+//    64-chunk of the type's list, and every row is tested against the chunk
+//    with ballot compaction.  Warps take items dynamically (load balance);
+//  * the accept decision is taken in fp32 wherever it is unambiguous: with
+//    r2f the fp32 squared displacement, r2f < lo2 accepts and r2f >= hi2
+//    rejects, where [lo2, hi2) brackets rs2 by more than the worst-case
+//    difference between r2f and the oracle's fp64 r2 (bound in list_args()).
+//    Pairs inside the band (~2e-3 per row) take the oracle's exact fp64 test
+//    on the raw coordinates, so the pair SET is bit-identical to the oracle's.
+// Rows come out ascending: candidates are staged in ascending atom order and a
+// row's chunks are visited in order by the one warp that owns the row.
+constexpr int kMaxRows = 256;   // atoms per cell handled by v4 (more -> overflow fallback)
+constexpr int kItemRows = 4;    // rows per work item
+constexpr int kMaxItems = kMaxRows / kItemRows + 8;
+
+// Rank, in ascending wrapped coordinate, of the neighbour at offset d in {-1,0,1}
+// of cell coordinate v (nc >= 3, so the three wrapped values are distinct).
+__device__ __forceinline__ int axis_rank(int v, int d, int nc) {
+    if (v == 0) return d == 0 ? 0 : (d == 1 ? 1 : 2);        // values 0, 1, nc-1
+    if (v == nc - 1) return d == 1 ? 0 : (d == -1 ? 1 : 2);  // values 0, nc-2, nc-1
+    return d + 1;
+}
+
+// bit tau set <=> the candidate lies within sqrt(rb2) of half-cell box tau
+// (tau = 4 bx + 2 by + bz, b = 0: [0, w/2), b = 1: [w/2, w) along the axis)
+__device__ __forceinline__ unsigned type_mask(const float4& f, float hw, float fw, float rb2) {
+    const float xl = fmaxf(fmaxf(-f.x, f.x - hw), 0.f), xu = fmaxf(fmaxf(hw - f.x, f.x - fw), 0.f);
+    const float yl = fmaxf(fmaxf(-f.y, f.y - hw), 0.f), yu = fmaxf(fmaxf(hw - f.y, f.y - fw), 0.f);
+    const float zl = fmaxf(fmaxf(-f.z, f.z - hw), 0.f), zu = fmaxf(fmaxf(hw - f.z, f.z - fw), 0.f);
+    const float ex[2] = {xl * xl, xu * xu}, ey[2] = {yl * yl, yu * yu}, ez[2] = {zl * zl, zu * zu};
+    unsigned tm = 0;
+#pragma unroll
+    for (int tau = 0; tau < 8; tau++) tm |= ((ex[tau >> 2] + ey[(tau >> 1) & 1] + ez[tau & 1]) < rb2 ? 1u : 0u) << tau;
+    return tm;
+}
+
+template <int DIRECT, int HALF>
+__global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
+    if (a.flags[0]) return;   // unwrapped input: the exact kernel (k_list_v2) builds the list
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned short* tl = reinterpret_cast<unsigned short*>(smem);            // [8][kMaxCand + 64] slot lists
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);   // (aliased) unsorted staging only
+    float4* C = reinterpret_cast<float4*>(smem + 8 * (kMaxCand + 64) * 2);   // [kMaxCand + 1], last = sentinel
+    unsigned char* TM = reinterpret_cast<unsigned char*>(C + (kMaxCand + 32));
+    __shared__ int64_t s_start[27];
+    __shared__ int s_off[28];
+    __shared__ signed char s_dc[27][3];   // neighbour cell offset (-1, 0, 1) per axis
+    __shared__ int s_any, s_unsorted, s_next;
+    __shared__ int s_tlen[8];
+    __shared__ float4 s_row[kMaxRows];
+    __shared__ unsigned char s_rtau[kMaxRows], s_rk[kMaxRows], s_rowlist[kMaxRows];
+    __shared__ int s_rcnt[8];
+    __shared__ int s_item[kMaxItems];
+    __shared__ int s_nitems;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int nc = a.cg.nc;
+    const double L = a.cg.L, halfL = 0.5 * a.cg.L;
+    const float hw = (float)(0.5 * a.w), fw = (float)a.w;
+    const unsigned lt = (1u << lane) - 1u;
+    constexpr int kTL = kMaxCand + 64;   // per-type list capacity
+    for (int64_t c = blockIdx.x; c < a.ncell; c += gridDim.x) {
+        const int64_t cs = a.start[c];
+        const int ccnt = (int)(a.start[c + 1] - cs);
+        __syncthreads();   // smem of the previous cell no longer in use
+        if (w == 0) {
+            // the 27 neighbour cells in ascending cell id: runs and offsets
+            const int ncz = (int)(c % nc), ncy = (int)((c / nc) % nc), ncx = (int)(c / ((int64_t)nc * nc));
+            int cnt = 0, rank = 31, first = 0, last = 0;
+            if (lane < 27) {
+                const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
+                int x = ncx + dx, y = ncy + dy, z = ncz + dz;
+                x += x < 0 ? nc : (x >= nc ? -nc : 0);
+                y += y < 0 ? nc : (y >= nc ? -nc : 0);
+                z += z < 0 ? nc : (z >= nc ? -nc : 0);
+                const int64_t cc = ((int64_t)x * nc + y) * nc + z;
+                const int64_t st = a.start[cc];
+                cnt = (int)(a.start[cc + 1] - st);
+                rank = axis_rank(ncx, dx, nc) * 9 + axis_rank(ncy, dy, nc) * 3 + axis_rank(ncz, dz, nc);
+                s_start[rank] = st;
+                s_dc[rank][0] = (signed char)dx;
+                s_dc[rank][1] = (signed char)dy;
+                s_dc[rank][2] = (signed char)dz;
+                s_off[rank + 1] = cnt;
+                if (cnt > 0) {
+                    first = a.atoms[st];
+                    last = a.atoms[st + cnt - 1];
+                }
+            }
+            bool mine = false;   // does this cell hold rows of [row_begin, row_end)?
+            for (int t = lane; t < ccnt; t += 32) {
+                const int i = a.atoms[cs + t];
+                mine |= i >= a.row_begin && i < a.row_end;
+            }
+            __syncwarp();
+            // in rank order: lane r handles the neighbour of rank r
+            const int mycnt = lane < 27 ? s_off[lane + 1] : 0;
+            int incl = mycnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            // first/last atom of the run of rank `lane` (lane `src` computed it)
+            int src = 0;
+#pragma unroll
+            for (int l = 0; l < 27; l++) src = (__shfl_sync(0xffffffffu, rank, l) == lane) ? l : src;
+            const int rf = __shfl_sync(0xffffffffu, first, src);
+            const int rl = __shfl_sync(0xffffffffu, last, src);
+            __syncwarp();
+            if (lane < 27) s_off[lane + 1] = incl;
+            if (lane == 0) s_off[0] = 0;
+            // candidates already ascending (atoms stored in cell order)?  Each cell's atoms
+            // are ascending (k_cell_sort_gather), so only run boundaries can break the order.
+            const unsigned ne = __ballot_sync(0xffffffffu, mycnt > 0);
+            const unsigned before = ne & lt;
+            const int prev = before ? 31 - __clz(before) : 0;
+            const int prev_last = __shfl_sync(0xffffffffu, rl, prev);
+            const unsigned bad = __ballot_sync(0xffffffffu, mycnt > 0 && before != 0 && prev_last > rf);
+            const unsigned any = __ballot_sync(0xffffffffu, mine);
+            if (lane == 0) {
+                s_unsorted = bad != 0;
+                s_any = any != 0;
+                s_next = 0;
+            }
+            if (lane < 8) s_rcnt[lane] = 0;
+        }
+        __syncthreads();
+        if (!s_any) continue;
+        const int M = s_off[27];
+        if (M > kMaxCand || ccnt > kMaxRows) {
+            if (!DIRECT && tid == 0) {
+                int k = atomicAdd(&a.n_overflow[0], 1);
+                a.overflow_cells[k] = (int)c;
+            }
+            continue;
+        }
+        const int M32 = (M + 31) & ~31;
+        if (!s_unsorted) {
+            // staging by runs: candidate k of run t is slot s_off[t] + k
+            for (int t = w; t < 27; t += kListWarps) {
+                const int n = s_off[t + 1] - s_off[t];
+                const float sx = s_dc[t][0] * fw, sy = s_dc[t][1] * fw, sz = s_dc[t][2] * fw;
+                const float4* src = a.qr_cell + s_start[t];
+                for (int k = lane; k < n; k += 32) {
+                    float4 f = src[k];
+                    f.x += sx;
+                    f.y += sy;
+                    f.z += sz;
+                    C[s_off[t] + k] = f;
+                    TM[s_off[t] + k] = (unsigned char)type_mask(f, hw, fw, a.rb2);
+                }
+            }
+        } else {
+            // general storage order: sort the staged keys (atom id, staging slot) first
+            for (int t = w; t < 27; t += kListWarps) {
+                const int n = s_off[t + 1] - s_off[t];
+                for (int k = lane; k < n; k += 32) {
+                    const int m = s_off[t] + k;
+                    key[m] = ((unsigned long long)(unsigned)a.atoms[s_start[t] + k] << 32) | (unsigned)m;
+                }
+            }
+            const int P = next_pow2(M);
+            for (int m = M + tid; m < P; m += blockDim.x) key[m] = ~0ull;
+            __syncthreads();
+            for (int k = 2; k <= P; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int idx = tid; idx < P; idx += blockDim.x) {
+                        const int ixj = idx ^ j;
+                        if (ixj > idx) {
+                            const unsigned long long x = key[idx], y = key[ixj];
+                            if ((x > y) == ((idx & k) == 0)) {
+                                key[idx] = y;
+                                key[ixj] = x;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int s = tid; s < M; s += blockDim.x) {
+                const int m = (int)(key[s] & 0xffffffffull);
+                int lo = 0, hi = 27;   // largest t with s_off[t] <= m
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_off[mid] <= m) lo = mid; else hi = mid;
+                }
+                float4 f = a.qr_cell[s_start[lo] + (m - s_off[lo])];
+                f.x += s_dc[lo][0] * fw;
+                f.y += s_dc[lo][1] * fw;
+                f.z += s_dc[lo][2] * fw;
+                C[s] = f;
+                TM[s] = (unsigned char)type_mask(f, hw, fw, a.rb2);
+            }
+        }
+        for (int s = M + tid; s < M32; s += blockDim.x) TM[s] = 0;
+        if (tid == 0) C[kMaxCand] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(-1));   // sentinel
+        // rows of this cell and their half-cell types
+        for (int t = tid; t < ccnt; t += blockDim.x) {
+            const float4 f = a.qr_cell[cs + t];
+            const int i = __float_as_int(f.w);
+            unsigned char tau = 255;
+            if (i >= a.row_begin && i < a.row_end) {
+                s_row[t] = f;
+                tau = (unsigned char)(((f.x >= hw) << 2) | ((f.y >= hw) << 1) | (f.z >= hw));
+                s_rk[t] = (unsigned char)atomicAdd(&s_rcnt[tau], 1);
+            }
+            s_rtau[t] = tau;
+        }
+        __syncthreads();
+        {   // warp w: the ordered slot list of type w, the rows of type w and its work items
+            const int tau = w;
+            unsigned short* lst = tl + tau * kTL;
+            int n = 0;
+            for (int ch = 0; ch < M32; ch += 32) {
+                const bool mem = (TM[ch + lane] >> tau) & 1u;
+                const unsigned m = __ballot_sync(0xffffffffu, mem);
+                if (mem) lst[n + __popc(m & lt)] = (unsigned short)(ch + lane);
+                n += __popc(m);
+            }
+            const int padded = (n + 63) & ~63;
+            for (int k = n + lane; k < padded; k += 32) lst[k] = (unsigned short)kMaxCand;
+            if (lane == 0) s_tlen[tau] = padded;
+            int rbase = 0, ibase = 0;
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int cu = s_rcnt[u];
+                if (u < tau) {
+                    rbase += cu;
+                    ibase += (cu + kItemRows - 1) / kItemRows;
+                }
+            }
+            for (int t = lane; t < ccnt; t += 32)
+                if (s_rtau[t] == tau) s_rowlist[rbase + s_rk[t]] = (unsigned char)t;
+            const int nr = s_rcnt[tau];
+            const int k = (nr + kItemRows - 1) / kItemRows;   // items of this type, sizes as equal as possible
+            if (lane < k) {
+                const int len = nr / k + (lane < nr % k ? 1 : 0);
+                const int u0 = lane * (nr / k) + min(lane, nr % k);
+                s_item[ibase + lane] = tau | ((rbase + u0) << 8) | (len << 16);
+            }
+            if (tau == 7 && lane == 0) s_nitems = ibase + k;
+        }
+        __syncthreads();
+        // work items: rows of one type (in registers) against the type's candidate list
+        for (;;) {
+            int it = 0;
+            if (lane == 0) it = atomicAdd(&s_next, 1);
+            it = __shfl_sync(0xffffffffu, it, 0);
+            if (it >= s_nitems) break;
+            const int code = s_item[it];
+            const int tau = code & 0xff, u0 = (code >> 8) & 0xff, nr = code >> 16;
+            float4 ri[kItemRows];
+            int32_t* dst[kItemRows];
+            int cur[kItemRows];
+#pragma unroll
+            for (int r = 0; r < kItemRows; r++) {
+                cur[r] = 0;
+                ri[r] = make_float4(3e30f, 3e30f, 3e30f, __int_as_float(-2));
+                dst[r] = a.out;
+                if (r < nr) {
+                    ri[r] = s_row[s_rowlist[u0 + r]];
+                    const int64_t rr = __float_as_int(ri[r].w) - a.row_begin;
+                    dst[r] = a.out + (DIRECT ? a.ptr[rr] : rr * (int64_t)kRowCap);
+                }
+            }
+            const unsigned short* lst = tl + tau * kTL;
+            const int len = s_tlen[tau];
+            for (int k0 = 0; k0 < len; k0 += 64) {
+                const float4 c0 = C[lst[k0 + lane]], c1 = C[lst[k0 + 32 + lane]];
+                const int j0 = __float_as_int(c0.w), j1 = __float_as_int(c1.w);
+#pragma unroll
+                for (int r = 0; r < kItemRows; r++) {
+                    if (r >= nr) break;
+                    const int i = __float_as_int(ri[r].w);
+                    float dx = c0.x - ri[r].x, dy = c0.y - ri[r].y, dz = c0.z - ri[r].z;
+                    const float r2a = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                    dx = c1.x - ri[r].x;
+                    dy = c1.y - ri[r].y;
+                    dz = c1.z - ri[r].z;
+                    const float r2b = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                    bool acc0 = r2a < a.lo2, acc1 = r2b < a.lo2;
+                    const bool band0 = !acc0 && r2a < a.hi2, band1 = !acc1 && r2b < a.hi2;
+                    if (__any_sync(0xffffffffu, band0 | band1)) {   // rare: the oracle's exact test
+                        if (band0) acc0 = dist2_exact(a.q[i], a.q[j0], L, halfL) < a.rs2;
+                        if (band1) acc1 = dist2_exact(a.q[i], a.q[j1], L, halfL) < a.rs2;
+                    }
+                    acc0 = acc0 && (HALF ? (j0 > i) : (j0 != i));
+                    acc1 = acc1 && (HALF ? (j1 > i) : (j1 != i));
+                    const unsigned m0 = __ballot_sync(0xffffffffu, acc0);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, acc1);
+                    const int p0 = cur[r] + __popc(m0 & lt);
+                    const int p1 = cur[r] + __popc(m0) + __popc(m1 & lt);
+                    if (acc0 && (DIRECT || p0 < kRowCap)) dst[r][p0] = j0;
+                    if (acc1 && (DIRECT || p1 < kRowCap)) dst[r][p1] = j1;
+                    cur[r] += __popc(m0) + __popc(m1);
+                }
+            }
+            if (!DIRECT) {
+#pragma unroll
+                for (int r = 0; r < kItemRows; r++) {
+                    if (r < nr && lane == r) {
+                        a.npart[__float_as_int(ri[r].w) - a.row_begin] = cur[r];
+                        if (cur[r] > kRowCap) atomicOr(&a.n_overflow[1], 1);
+                    }
+                }
+            }
+        }
+    }
+}
+
 // Fallback for cells with more than kMaxCand candidates (dense or tiny boxes):
 // one warp per row straight from global memory, per-row bitonic sort.
 template <int DIRECT>
@@ -655,10 +999,14 @@ BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows) {
     o = align256(o + sizeof(rec4) * (size_t)n);
     W.off_qf = o;
     o = align256(o + sizeof(float4) * (size_t)n);
+    W.off_qr = o;
+    o = align256(o + sizeof(float4) * (size_t)n);
     W.off_scan = o;
     o = align256(o + sizeof(int64_t) * (size_t)(W.scan_blocks + 1));
     W.off_over = o;    // [0] overflow cell count, [1] row overflow flag, then ncell cell ids
     o = align256(o + sizeof(int32_t) * (size_t)(ncell + 2));
+    W.off_flags = o;   // [0] some raw coordinate outside [0, L) (set by k_cell_assign)
+    o = align256(o + sizeof(int32_t) * 4);
     W.off_ptrtmp = o;  // rows + 1 int64 (padded layout: scan of the counts)
     o = align256(o + sizeof(int64_t) * (size_t)(rows + 1));
     W.off_scratch = o; // rows * kRowCap int32
@@ -688,29 +1036,57 @@ cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* w
     int32_t* atoms = (int32_t*)(ws + W.off_atoms);
     rec4* q_cell = (rec4*)(ws + W.off_qcell);
     float4* qf_cell = (float4*)(ws + W.off_qf);
+    float4* qr_cell = (float4*)(ws + W.off_qr);
     int64_t* scan = (int64_t*)(ws + W.off_scan);
     cudaError_t e;
     if ((e = cudaMemsetAsync(count, 0, sizeof(int32_t) * (size_t)cg.ncell, s)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (size_t)cg.ncell, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ws + W.off_flags, 0, sizeof(int32_t) * 4, s)) != cudaSuccess) return e;
     if (n > 0) {
-        k_cell_assign<<<grid_for(n, 256), 256, 0, s>>>((const rec4*)q, n, cg, cell_of, count);
+        k_cell_assign<<<grid_for(n, 256), 256, 0, s>>>((const rec4*)q, n, cg, cell_of, count,
+                                                       (int32_t*)(ws + W.off_flags));
         g_launches++;
     }
     if ((e = launch_scan_i32_to_i64(count, start, cg.ncell, scan, W.scan_blocks, s)) != cudaSuccess) return e;
     if (n > 0) {
         k_cell_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, cell_of, start, cursor, atoms);
         k_cell_sort_gather<<<grid_for(cg.ncell, kListWarps), kListWarps * 32, 0, s>>>((const rec4*)q, cg, start,
-                                                                                     atoms, q_cell, qf_cell);
+                                                                                     atoms, q_cell, qf_cell, qr_cell,
+                                                                                     cg.L / cg.nc);
         g_launches += 2;
     }
     return cudaGetLastError();
 }
 
-static ListArgs list_args(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end, int32_t* npart,
-                          const int64_t* ptr, int32_t* out, char* ws, const BuildWorkspace& W) {
+static ListArgs list_args(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
+                          int64_t row_end, int32_t* npart, const int64_t* ptr, int32_t* out, char* ws,
+                          const BuildWorkspace& W) {
     ListArgs a;
+    a.q = (const rec4*)q;
+    a.flags = (const int32_t*)(ws + W.off_flags);
+    a.w = cg.L / cg.nc;
+    {
+        // v4 fp32 decision band.  A staged coordinate is u = fl32(x - o_own) + k fl32(w)
+        // (k in {-1,0,1}: the neighbour cell's offset), |u| <= X = 2w + rs, carrying at most
+        // 2^-24 (w + w + 2w) of rounding; a row coordinate carries <= 2^-24 w.  So each
+        // fp32 displacement differs from the oracle's fp64 minimum-image displacement by
+        //   eps_d <= 2^-22 X + 2^-24 rs (the fp32 subtraction near |d| ~ rs)
+        //            + 2^-49 L (fp64 roundings of x - o and of the oracle's d, both sides).
+        // Near r2 ~ rs2 the fp32 r2 (3 roundings) then differs from the oracle's r2 by
+        // at most 2 sqrt(3) rs eps_d + 4 * 2^-24 rs2 (+ the oracle's own 2^-52 rs2);
+        // the band takes 4x that.
+        const double X = 2.0 * a.w + rs;
+        const double eps_d = std::ldexp(X, -22) + std::ldexp(rs, -24) + std::ldexp(cg.L, -49);
+        const double rs2 = rs * rs;
+        const double delta = 4.0 * (2.0 * std::sqrt(3.0) * rs * eps_d + std::ldexp(4.0 * rs2, -24)) + 1e-9 * rs2;
+        a.lo2 = std::nextafter((float)(rs2 - delta), 0.0f);
+        a.hi2 = std::nextafter((float)(rs2 + delta), INFINITY);
+        const double rb = rs * (1.0 + 1e-4) + 1e-4;   // covers fp32 coordinate errors and edge rows
+        a.rb2 = std::nextafter((float)(rb * rb), INFINITY);
+    }
     a.q_cell = (const rec4*)(ws + W.off_qcell);
     a.qf_cell = (const float4*)(ws + W.off_qf);
+    a.qr_cell = (const float4*)(ws + W.off_qr);
     a.atoms = (const int32_t*)(ws + W.off_atoms);
     a.start = (const int64_t*)(ws + W.off_start);
     a.ncell = cg.ncell;
@@ -738,9 +1114,9 @@ static int list_grid(const CellGrid& cg, int per_sm) {
 }
 
 constexpr size_t kListSmem = (size_t)kMaxCand * 8 + (size_t)(kMaxCand + 32) * (3 * 8 + 4 + 1);
+constexpr size_t kListSmemV4 = (size_t)8 * (kMaxCand + 64) * 2 + (size_t)(kMaxCand + 32) * (16 + 1);
 
-cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
-                              int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W, cudaStream_t s) {
+static cudaError_t set_list_attrs() {
     static bool attr = false;
     if (!attr) {
         void (*fns[4])(ListArgs) = {k_list_v2<0, 0>, k_list_v2<0, 1>, k_list_v2<1, 0>, k_list_v2<1, 1>};
@@ -748,26 +1124,49 @@ cudaError_t launch_list_pass1(const CellGrid& cg, double rs, int half, int64_t r
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
             if (e != cudaSuccess) return e;
         }
+        void (*fns4[4])(ListArgs) = {k_list_v4<0, 0>, k_list_v4<0, 1>, k_list_v4<1, 0>, k_list_v4<1, 1>};
+        for (auto f : fns4) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmemV4);
+            if (e != cudaSuccess) return e;
+        }
         attr = true;
     }
-    ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, nullptr,
-                           out ? out : (int32_t*)(ws + W.off_scratch), ws, W);
-    cudaError_t e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
+    return cudaSuccess;
+}
+
+// The exact kernel (v2/v3) and the fast kernel (v4) are both launched; each
+// returns at once unless the input-range flag of k_cell_assign selects it.
+template <int DIRECT>
+static void launch_list_kernels(const ListArgs& a, const CellGrid& cg, int half, cudaStream_t s) {
+    if (half) {
+        k_list_v4<DIRECT, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmemV4, s>>>(a);
+        k_list_v2<DIRECT, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
+    } else {
+        k_list_v4<DIRECT, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmemV4, s>>>(a);
+        k_list_v2<DIRECT, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
+    }
+    k_list_fallback<DIRECT><<<148, kListWarps * 32, 0, s>>>(a);
+    g_launches += 3;
+}
+
+cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
+                              int64_t row_end, int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W,
+                              cudaStream_t s) {
+    cudaError_t e = set_list_attrs();
     if (e != cudaSuccess) return e;
-    if (half)
-        k_list_v2<0, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
-    else
-        k_list_v2<0, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
-    k_list_fallback<0><<<148, kListWarps * 32, 0, s>>>(a);
-    g_launches += 2;
+    ListArgs a = list_args(q, cg, rs, half, row_begin, row_end, npart, nullptr,
+                           out ? out : (int32_t*)(ws + W.off_scratch), ws, W);
+    e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    launch_list_kernels<0>(a, cg, half, s);
     return cudaGetLastError();
 }
 
 const int32_t* list_row_overflow_flag(char* ws, const BuildWorkspace& W) { return (const int32_t*)(ws + W.off_over) + 1; }
 
-cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t row_begin, int64_t row_end,
-                              int32_t* npart, const int64_t* ptr, int32_t* list, bool row_overflow, char* ws,
-                              const BuildWorkspace& W, cudaStream_t s) {
+cudaError_t launch_list_pass2(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
+                              int64_t row_end, int32_t* npart, const int64_t* ptr, int32_t* list, bool row_overflow,
+                              char* ws, const BuildWorkspace& W, cudaStream_t s) {
     const int64_t rows = row_end - row_begin;
     if (!row_overflow) {
         k_compact<<<grid_for(rows * 32, 256, 148 * 32), 256, 0, s>>>((const int32_t*)(ws + W.off_scratch), npart, ptr,
@@ -775,13 +1174,10 @@ cudaError_t launch_list_pass2(const CellGrid& cg, double rs, int half, int64_t r
         g_launches++;
         return cudaGetLastError();
     }
-    ListArgs a = list_args(cg, rs, half, row_begin, row_end, npart, ptr, list, ws, W);
-    if (half)
-        k_list_v2<1, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
-    else
-        k_list_v2<1, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
-    k_list_fallback<1><<<148, kListWarps * 32, 0, s>>>(a);
-    g_launches += 2;
+    cudaError_t e = set_list_attrs();
+    if (e != cudaSuccess) return e;
+    ListArgs a = list_args(q, cg, rs, half, row_begin, row_end, npart, ptr, list, ws, W);
+    launch_list_kernels<1>(a, cg, half, s);
     return cudaGetLastError();
 }
 

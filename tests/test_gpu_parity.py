@@ -109,6 +109,35 @@ def test_list_unwrapped_positions(lj, dev, systems):
     assert_same_list(gl, oracle.list_cells(q, w.L, w.rs, False))
 
 
+@pytest.mark.parametrize("half", [True, False])
+def test_list_pairs_at_the_search_radius(lj, dev, half):
+    """Pairs whose distance is within a few ulps (up to 1e-6) of r_s, in every
+    direction and across the periodic faces: the fast builder decides these in
+    its exact fp64 band (reading C-4: strict r2 < rs*rs) -- the pair set must
+    still equal the oracle's."""
+    rs, L = 3.3, 40.0
+    rng = np.random.default_rng(11)
+    offs = [-1e-6, -1e-9, -1e-12, -4e-15, 0.0, 4e-15, 1e-12, 1e-9, 1e-6]
+    pts = []
+    centres = [(x, y, z) for x in range(5) for y in range(5) for z in range(5)]
+    for k, (x, y, z) in enumerate(centres):
+        c = (np.array([x, y, z]) + 0.5) * 8.0 + rng.uniform(-0.5, 0.5, 3)
+        if k % 7 == 0:   # straddle a box face
+            c[k % 3] = 0.3
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        d = rs + offs[k % len(offs)]
+        a, b = c - 0.5 * d * u, c + 0.5 * d * u
+        pts += [np.mod(a, L), np.mod(b, L)]
+    q = np.ascontiguousarray(np.array(pts))
+    q = np.where(q >= L, q - L, q)
+    g = lj.geom(L, 3.0, rs)
+    gl = lj.build_list(to_dev(q, dev), g, half)
+    ol = oracle.list_cells(q, L, rs, half)
+    assert ol.n_entries > 0
+    assert_same_list(gl, ol)
+
+
 def test_list_capacity_protocol(lj, dev, systems):
     w = systems[1]
     g = lj.geom(w.L, w.rc, w.rs)

@@ -1,0 +1,47 @@
+"""List-build timing on one GPU (development tool): compact and padded layouts,
+configs 3 (cell order) and 4 (cell order).  One JSON object per measurement."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import lj_inputs  # noqa: E402
+from paper_1806_05713_b200 import lj  # noqa: E402
+
+
+def timeit(fn, reps=10, warm=2):
+    for _ in range(warm):
+        fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    dev = torch.device("cuda:0")
+    for c in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3,4").split(",")]:
+        w = lj_inputs.config(c)
+        g = lj.geom(w.L, w.rc, w.rs)
+        q = lj.pack_aos4(torch.from_numpy(w.q).to(dev))
+        perm = lj.cell_order(q, g)
+        q = lj.permute_rows(q, perm)
+        for padded in (False, True):
+            for half in ((False, True) if c < 4 else (False,)):
+                b = lj.ListBuilder(w.n, g, half, device=dev, padded=padded)
+                lst = b.build(q)
+                ms = timeit(lambda: b.build(q))
+                print(json.dumps(dict(cfg=c, half=half, padded=padded, what="build", ms=round(ms, 4),
+                                      entries=lst.n_entries)), flush=True)
+                del b, lst
+                torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
