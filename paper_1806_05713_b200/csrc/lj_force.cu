@@ -38,6 +38,7 @@ struct PairConsts {
     double c48, c24; // 48 dt, 24 dt
     long long rc2_bits;
     int hi_halfL;    // high word of L/2 (INT_MAX for open boundaries)
+    int hi_L2q;      // high word of (L/2)^2: r^2 below it needs no image (INT_MAX for open boundaries)
 };
 
 __device__ __forceinline__ double fast_rcp(double x) {
@@ -56,27 +57,6 @@ __device__ __forceinline__ double image_shift(double d, double L, int hi_halfL) 
     int hi = __double2hiint(d);
     double s = ((hi & 0x7fffffff) > hi_halfL) ? L : 0.0;
     return hi < 0 ? -s : s;
-}
-
-// One list entry: returns the impulse coefficient df (0 if r >= r_c) and the
-// minimum-image relative vector in dx, dy, dz.
-__device__ __forceinline__ double pair_df(const rec4& qi, const rec4& qj, const PairConsts& c, double& dx, double& dy,
-                                          double& dz, bool& inside) {
-    dx = qj.x - qi.x;
-    dy = qj.y - qi.y;
-    dz = qj.z - qi.z;
-    bool need = beyond_half(dx, c.hi_halfL) | beyond_half(dy, c.hi_halfL) | beyond_half(dz, c.hi_halfL);
-    if (__any_sync(__activemask(), need)) {
-        dx -= image_shift(dx, c.L, c.hi_halfL);
-        dy -= image_shift(dy, c.L, c.hi_halfL);
-        dz -= image_shift(dz, c.L, c.hi_halfL);
-    }
-    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    double inv2 = fast_rcp(r2);
-    double inv6 = inv2 * inv2 * inv2;
-    double df = fma(c.c48, inv6, -c.c24) * (inv6 * inv2);
-    inside = __double_as_longlong(r2) < c.rc2_bits;
-    return inside ? df : 0.0;
 }
 
 template <int G>
@@ -100,6 +80,11 @@ __device__ __forceinline__ void count_interactions(unsigned cnt, unsigned long l
 // G lanes per row, U independent partner gathers in flight per lane.
 // Full list: no atomics, p_i committed once by lane 0 of the group.
 // Half list: p_j += df r by fp64 REDs, p_i committed by REDs as well.
+// The chunk loop runs while ANY row of the warp has entries left (warp-uniform
+// trip count), so the minimum-image test can be one vote per chunk: r^2 of the
+// raw differences below (L/2)^2 (integer test on the high words) proves that no
+// component needs an image; otherwise (rows near a box face) the differences
+// are corrected per component and r^2 recomputed.
 template <int G, int U, bool HALF>
 __global__ void __launch_bounds__(kForceThreads)
     k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
@@ -111,52 +96,73 @@ __global__ void __launch_bounds__(kForceThreads)
     const bool active = r < rows;
     double ax = 0.0, ay = 0.0, az = 0.0;
     unsigned cnt = 0;
-    if (active) {
-        const int64_t i = row_begin + r;
-        const rec4 qi = load_rec(q, i);
-        const int32_t* __restrict__ lst = list + ptr[r];
-        const int n = npart[r];
-        // software pipeline (the GPU analogue of the paper's SWP): the
-        // indices of chunk k+1 are loaded before the records of chunk k are used
-        int jn[U];
+    const int64_t i = row_begin + (active ? r : 0);
+    const rec4 qi = load_rec(q, active ? i : 0);
+    const int32_t* __restrict__ lst = list + (active ? ptr[r] : 0);
+    const int n = active ? npart[r] : 0;
+    // software pipeline (the GPU analogue of the paper's SWP): the
+    // indices of chunk k+1 are loaded before the records of chunk k are used
+    int jn[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
-        for (int k0 = g; k0 < n; k0 += U * G) {
-            int j[U];
-            rec4 qj[U];
+    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
+    for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
+        int j[U];
+        rec4 qj[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) j[u] = jn[u];
+        for (int u = 0; u < U; u++) {
+            j[u] = jn[u];
+            qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);   // no entry: r = 0, masked below
+        }
 #pragma unroll
-            for (int u = 0; u < U; u++)
-                if (j[u] >= 0) qj[u] = load_rec(q, j[u]);
+        for (int u = 0; u < U; u++) {
+            const int kn = k0 + U * G + u * G;
+            jn[u] = kn < n ? __ldg(lst + kn) : -1;
+        }
+        double dx[U], dy[U], dz[U], r2[U];
+        int hmax = 0;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            dx[u] = qj[u].x - qi.x;
+            dy[u] = qj[u].y - qi.y;
+            dz[u] = qj[u].z - qi.z;
+            r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+            hmax = max(hmax, __double2hiint(r2[u]));
+        }
+        auto accumulate = [&]() {
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const int kn = k0 + U * G + u * G;
-                jn[u] = kn < n ? __ldg(lst + kn) : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if (j[u] >= 0) {
-                    double dx, dy, dz;
-                    bool in;
-                    const double df = pair_df(qi, qj[u], c, dx, dy, dz, in);
-                    ax = fma(-df, dx, ax);
-                    ay = fma(-df, dy, ay);
-                    az = fma(-df, dz, az);
-                    cnt += in;
-                    if (HALF && in) {
-                        atomicAdd(&p[j[u]].x, df * dx);
-                        atomicAdd(&p[j[u]].y, df * dy);
-                        atomicAdd(&p[j[u]].z, df * dz);
-                    }
+                const double inv2 = fast_rcp(r2[u]);
+                const double inv6 = inv2 * inv2 * inv2;
+                const bool in = j[u] >= 0 && __double_as_longlong(r2[u]) < c.rc2_bits;
+                const double df = in ? fma(c.c48, inv6, -c.c24) * (inv6 * inv2) : 0.0;
+                ax = fma(-df, dx[u], ax);
+                ay = fma(-df, dy[u], ay);
+                az = fma(-df, dz[u], az);
+                cnt += in;
+                if (HALF && in) {
+                    atomicAdd(&p[j[u]].x, df * dx[u]);
+                    atomicAdd(&p[j[u]].y, df * dy[u]);
+                    atomicAdd(&p[j[u]].z, df * dz[u]);
                 }
             }
+        };
+        // (the tail is duplicated in both branches so that the common path keeps r^2)
+        if (__any_sync(0xffffffffu, hmax >= c.hi_L2q)) {   // some pair may need a periodic image
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                dx[u] -= image_shift(dx[u], c.L, c.hi_halfL);
+                dy[u] -= image_shift(dy[u], c.L, c.hi_halfL);
+                dz[u] -= image_shift(dz[u], c.L, c.hi_halfL);
+                r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+            }
+            accumulate();
+        } else {
+            accumulate();
         }
     }
     unsigned cnt_row = cnt;
     group_reduce<G>(ax, ay, az, cnt_row);
     if (active && g == 0) {
-        const int64_t i = row_begin + r;
         if (HALF) {
             // p_i is concurrently a RED target of earlier rows (i in row(i'), i' < i):
             // commit with REDs too (SURVEY §8(a) a6 race hazard).
@@ -248,6 +254,7 @@ __global__ void __launch_bounds__(kForceThreads)
     count_interactions(cnt, n_inter);
 }
 
+
 PairConsts make_consts(const ForceArgs& a) {
     PairConsts c;
     c.L = a.L;
@@ -262,8 +269,11 @@ PairConsts make_consts(const ForceArgs& a) {
     if (a.L > 0.0) {
         u.d = 0.5 * a.L;
         c.hi_halfL = (int)(u.b >> 32);
+        u.d = 0.25 * a.L * a.L;
+        c.hi_L2q = (int)(u.b >> 32);
     } else {
         c.hi_halfL = INT_MAX;
+        c.hi_L2q = INT_MAX;
     }
     return c;
 }
