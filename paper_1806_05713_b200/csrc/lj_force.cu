@@ -85,8 +85,10 @@ __device__ __forceinline__ void count_interactions(unsigned cnt, unsigned long l
 // raw differences below (L/2)^2 (integer test on the high words) proves that no
 // component needs an image; otherwise (rows near a box face) the differences
 // are corrected per component and r^2 recomputed.
+// U = 2: at most 48 registers -> 5 CTAs (40 warps) per SM; measured 0.79 vs 0.83 ms
+// (54 registers, 4 CTAs) on config 4 -- the kernel is latency/L1-bound, warps help.
 template <int G, int U, bool HALF>
-__global__ void __launch_bounds__(kForceThreads)
+__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : 3)
     k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
             const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
             PairConsts c, unsigned long long* n_inter) {

@@ -149,6 +149,7 @@ class CSRList:
     row_begin: int
     row_end: int
     half: bool
+    padded: bool = False   # LJ_LIST_PADDED layout (rows at a fixed stride)
 
     @property
     def rows(self):
@@ -201,7 +202,7 @@ class ListBuilder:
         self.rebuilds += 1
         rows = self.row_end - self.row_begin
         return CSRList(self.npart[:rows], self.pointer, self.sorted_list, int(ne.value), self.row_begin,
-                       self.row_end, self.half)
+                       self.row_end, self.half, self.padded)
 
 
 def build_list(q: torch.Tensor, g: Geom, half: bool, row_begin: int = 0, row_end: int | None = None) -> CSRList:
@@ -244,6 +245,8 @@ def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRLis
     _rec(p, "p")
     if n_interactions is not None and not (n_interactions.is_cuda and n_interactions.dtype == torch.int64):
         raise TypeError("n_interactions must be a CUDA int64 tensor")
+    if lanes_per_row == 0 and lst.padded and not lst.half and not ordered:
+        lanes_per_row = 8 | (2 << 8)   # padded rows: 8 lanes per row measured faster (0.82 vs 0.87 ms, config 4)
     _check(load().lj_force_step_ex(_ptr(q), _ptr(p), q.shape[0], g, float(dt), int(lst.half), *_list_args(lst),
                                    int(lanes_per_row), int(ordered), _ptr(n_interactions), _stream()))
 
