@@ -1,6 +1,6 @@
-"""Force / build timing vs storage order on one GPU (development tool): config 4
-(or argv[1]) re-sorted into cell order and into the fine (sub-cell Morton) cell
-order; padded and compact lists; 4 and 8 lanes per row."""
+"""Force / build timing on one GPU (development tool): config 4 (or argv[1])
+re-sorted into cell order; padded and compact lists; 4 and 8 lanes per row;
+the gather probe."""
 import json
 import os
 import sys
@@ -32,8 +32,8 @@ def main():
     g = lj.geom(w.L, w.rc, w.rs)
     q0 = lj.pack_aos4(torch.from_numpy(w.q).to(dev))
     p = lj.pack_aos4(torch.from_numpy(w.p).to(dev))
-    for fine in (False, True):
-        q = lj.permute_rows(q0, lj.cell_order(q0, g, fine=fine))
+    for fine in (False,):
+        q = lj.permute_rows(q0, lj.cell_order(q0, g))
         for padded in (True, False):
             b = lj.ListBuilder(w.n, g, False, device=dev, padded=padded)
             lst = b.build(q)
