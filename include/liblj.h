@@ -103,6 +103,21 @@ lj_status lj_build_list_ex(const double *q, int64_t n, lj_geom g, int half, int6
                            int64_t capacity, int64_t *n_entries, void *workspace, size_t workspace_bytes,
                            void *stream);
 
+/* Fused bookkeeping rebuild (PAPER.md:190-192 with the config-3 reordering):
+ * wrap q into [0,L) in place (as lj_wrap), perm = the cell order of the wrapped
+ * q (as lj_cell_order), q_out = q[perm], p_out = p[perm] (skipped if p == NULL),
+ * q_ref = q_out (skipped if NULL), and the list of rows [row_begin, row_end) of
+ * the PERMUTED system q_out -- every output bit-identical to lj_wrap +
+ * lj_cell_order + lj_permute_rows + lj_build_list_ex(q_out, ...), from a single
+ * cell pass.  Outputs must not alias inputs or each other.  List arguments,
+ * flags, capacity protocol and synchronisation as lj_build_list_ex (a repeated
+ * call after LJ_ERR_CAPACITY with the same arguments is valid: wrapping is
+ * idempotent). */
+lj_status lj_rebuild(double *q, const double *p, double *q_out, double *p_out, double *q_ref, int64_t *perm,
+                     int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end, int flags,
+                     int32_t *number_of_partners, int64_t *pointer, int32_t *sorted_list, int64_t capacity,
+                     int64_t *n_entries, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Spatial reordering (BASELINE.json config 3): perm[new] = old, the stable
  * sort of the atoms by cell id (cx*nc + cy)*nc + cz (same cells as the list). */
 lj_status lj_cell_order(const double *q, int64_t n, lj_geom g, int64_t *perm,

@@ -125,10 +125,21 @@ lj_status lj_build_list_workspace(int64_t n, lj_geom g, size_t* bytes) {
     return LJ_OK;
 }
 
-lj_status lj_build_list_ex(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
-                           int flags, int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list,
-                           int64_t capacity, int64_t* n_entries, void* workspace, size_t workspace_bytes,
-                           void* stream) {
+namespace {
+// What precedes the list passes: the plain cell pass over q (lj_build_list) or
+// the fused wrap + cells + permutation of lj_rebuild (the list is then built
+// over q_out, the permuted system).
+struct RebuildIO {
+    double* q;   // wrapped in place
+    const double* p;
+    double *q_out, *p_out, *q_ref;
+    int64_t* perm;
+};
+
+lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
+                          int flags, int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list,
+                          int64_t capacity, int64_t* n_entries, void* workspace, size_t workspace_bytes,
+                          void* stream, const RebuildIO* rb) {
     LJ_TRY(check_n(n));
     LJ_TRY(check_geom(g, true));
     LJ_TRY(check_rows(n, row_begin, row_end));
@@ -153,7 +164,11 @@ lj_status lj_build_list_ex(const double* q, int64_t n, lj_geom g, int half, int6
         return fail(LJ_ERR_CAPACITY, "build_list: padded layout needs capacity %lld", (long long)*n_entries);
     }
     int64_t* counts_scan = padded ? (int64_t*)(ws + W.off_ptrtmp) : pointer;
-    LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
+    if (rb)
+        LJ_CUDA(launch_rebuild_cells(rb->q, rb->p, rb->q_out, rb->p_out, rb->q_ref, rb->perm, n, cg, ws, W, s),
+                "lj_rebuild/cells");
+    else
+        LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
     if (rows > 0)
         LJ_CUDA(launch_list_pass1(q, cg, g.rs, half, row_begin, row_end, number_of_partners,
                                   padded ? sorted_list : nullptr, ws, W, s),
@@ -186,6 +201,30 @@ lj_status lj_build_list_ex(const double* q, int64_t n, lj_geom g, int half, int6
                                   row_overflow != 0, ws, W, s),
                 "lj_build_list/pass2");
     return LJ_OK;
+}
+
+}  // namespace
+
+lj_status lj_build_list_ex(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
+                           int flags, int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list,
+                           int64_t capacity, int64_t* n_entries, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+    return build_list_impl(q, n, g, half, row_begin, row_end, flags, number_of_partners, pointer, sorted_list,
+                           capacity, n_entries, workspace, workspace_bytes, stream, nullptr);
+}
+
+lj_status lj_rebuild(double* q, const double* p, double* q_out, double* p_out, double* q_ref, int64_t* perm,
+                     int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end, int flags,
+                     int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list, int64_t capacity,
+                     int64_t* n_entries, void* workspace, size_t workspace_bytes, void* stream) {
+    if (n > 0 && (!q || !q_out || !perm || (p && !p_out))) return fail(LJ_ERR_ARG, "rebuild: null pointer");
+    if (n > 0 && (q_out == q || (p && (p_out == p || p_out == q_out)) || q_ref == q || q_ref == q_out))
+        return fail(LJ_ERR_ARG, "rebuild: output buffers must be distinct from the inputs and each other");
+    if (!aligned32(q) || !aligned32(q_out) || !aligned32(p) || !aligned32(p_out) || !aligned32(q_ref))
+        return fail(LJ_ERR_ARG, "rebuild: records not 32-byte aligned");
+    RebuildIO io{q, p, q_out, p_out, q_ref, perm};
+    return build_list_impl(q_out, n, g, half, row_begin, row_end, flags, number_of_partners, pointer, sorted_list,
+                           capacity, n_entries, workspace, workspace_bytes, stream, &io);
 }
 
 lj_status lj_build_list(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,

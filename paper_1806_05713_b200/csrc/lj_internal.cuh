@@ -48,6 +48,11 @@ BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows);
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* ws, const BuildWorkspace& W,
                          cudaStream_t s);
+// lj_rebuild: wrap q in place, cells, and the cell-order permutation applied to q/p (q_out, p_out, q_ref), with
+// the builder's staging arrays prepared for the permuted system
+cudaError_t launch_rebuild_cells(double* q, const double* p, double* q_out, double* p_out, double* q_ref,
+                                 int64_t* perm, int64_t n, const CellGrid& cg, char* ws, const BuildWorkspace& W,
+                                 cudaStream_t s);
 // pass 1: every row into the per-row scratch (stride kRowCap), counts into npart
 // (out == nullptr: the workspace scratch; else the caller's padded list)
 cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,

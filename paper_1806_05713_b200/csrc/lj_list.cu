@@ -172,6 +172,76 @@ __global__ void k_cell_sort_gather(const rec4* __restrict__ q, CellGrid cg, cons
     }
 }
 
+// ---- fused rebuild (lj_rebuild): wrap + cells + cell-order permutation -------
+
+// Wrap q into [0, L) in place (reading C-3, as lj_wrap) and assign cells.
+__global__ void k_wrap_assign(rec4* __restrict__ q, int64_t n, CellGrid cg, int32_t* __restrict__ cell_of,
+                              int32_t* __restrict__ count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        rec4 r = q[i];
+        r.x = wrap_exact(r.x, cg.L);
+        r.y = wrap_exact(r.y, cg.L);
+        r.z = wrap_exact(r.z, cg.L);
+        q[i] = r;
+        const int cx = cell_coord(r.x, cg), cy = cell_coord(r.y, cg), cz = cell_coord(r.z, cg);
+        const int c = (cx * cg.nc + cy) * cg.nc + cz;
+        cell_of[i] = c;
+        atomicAdd(&count[c], 1);
+    }
+}
+
+// One warp per cell: sort the cell's atoms ascending (= lj_cell_order's stable
+// sort by cell id), then emit the permutation and the permuted records
+// (q_out, p_out, q_ref) and the builder's staging arrays for the NEW storage
+// order (atoms = identity, q_cell = q_out, qr_cell), so the list kernels run
+// on the permuted system without a second cell pass.
+__global__ void k_cell_sort_permute(const rec4* __restrict__ q, const rec4* __restrict__ p, CellGrid cg,
+                                    const int64_t* __restrict__ start, int32_t* __restrict__ atoms,
+                                    int64_t* __restrict__ perm, rec4* __restrict__ q_out, rec4* __restrict__ p_out,
+                                    rec4* __restrict__ q_ref, rec4* __restrict__ q_cell,
+                                    float4* __restrict__ qr_cell, double cw) {
+    const int64_t ncell = cg.ncell;
+    __shared__ int buf[kListWarps][kCellBuf];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t c = blockIdx.x * (int64_t)kListWarps + w; c < ncell; c += (int64_t)gridDim.x * kListWarps) {
+        const int64_t s = start[c];
+        const int cnt = (int)(start[c + 1] - s);
+        if (cnt <= kCellBuf) {
+            const int P = next_pow2(cnt);
+            for (int k = lane; k < P; k += 32) buf[w][k] = k < cnt ? atoms[s + k] : INT_MAX;
+            __syncwarp();
+            warp_bitonic_sort(buf[w], P, lane);
+            for (int k = lane; k < cnt; k += 32) atoms[s + k] = buf[w][k];
+            __syncwarp();
+        } else if (lane == 0) {   // pathological cell occupancy: insertion sort in place
+            for (int a = 1; a < cnt; a++) {
+                int v = atoms[s + a], b = a - 1;
+                while (b >= 0 && atoms[s + b] > v) {
+                    atoms[s + b + 1] = atoms[s + b];
+                    b--;
+                }
+                atoms[s + b + 1] = v;
+            }
+        }
+        __syncwarp();
+        const int cz = (int)(c % cg.nc), cy = (int)((c / cg.nc) % cg.nc), cx = (int)(c / ((int64_t)cg.nc * cg.nc));
+        const double ox = cx * cw, oy = cy * cw, oz = cz * cw;
+        for (int k = lane; k < cnt; k += 32) {
+            const int64_t g = s + k;
+            const int i = atoms[g];
+            const rec4 r = q[i];
+            perm[g] = i;
+            q_out[g] = r;
+            q_cell[g] = r;
+            if (q_ref) q_ref[g] = r;
+            if (p) p_out[g] = p[i];
+            qr_cell[g] = make_float4((float)(r.x - ox), (float)(r.y - oy), (float)(r.z - oz), __int_as_float((int)g));
+        }
+        __syncwarp();
+        for (int k = lane; k < cnt; k += 32) atoms[s + k] = (int32_t)(s + k);   // new order: identity
+    }
+}
+
 // ---- list ----------------------------------------------------------------
 
 // Neighbour cell t (0..26) of cell c: start, count and the periodic shift that
@@ -1053,6 +1123,35 @@ cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* w
         k_cell_sort_gather<<<grid_for(cg.ncell, kListWarps), kListWarps * 32, 0, s>>>((const rec4*)q, cg, start,
                                                                                      atoms, q_cell, qf_cell, qr_cell,
                                                                                      cg.L / cg.nc);
+        g_launches += 2;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rebuild_cells(double* q, const double* p, double* q_out, double* p_out, double* q_ref,
+                                 int64_t* perm, int64_t n, const CellGrid& cg, char* ws, const BuildWorkspace& W,
+                                 cudaStream_t s) {
+    int32_t* cell_of = (int32_t*)(ws + W.off_cell_of);
+    int32_t* count = (int32_t*)(ws + W.off_count);
+    int64_t* start = (int64_t*)(ws + W.off_start);
+    int32_t* cursor = (int32_t*)(ws + W.off_cursor);
+    int32_t* atoms = (int32_t*)(ws + W.off_atoms);
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(count, 0, sizeof(int32_t) * (size_t)cg.ncell, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (size_t)cg.ncell, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ws + W.off_flags, 0, sizeof(int32_t) * 4, s)) != cudaSuccess) return e;   // wrapped input
+    if (n > 0) {
+        k_wrap_assign<<<grid_for(n, 256), 256, 0, s>>>((rec4*)q, n, cg, cell_of, count);
+        g_launches++;
+    }
+    if ((e = launch_scan_i32_to_i64(count, start, cg.ncell, (int64_t*)(ws + W.off_scan), W.scan_blocks, s)) !=
+        cudaSuccess)
+        return e;
+    if (n > 0) {
+        k_cell_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, cell_of, start, cursor, atoms);
+        k_cell_sort_permute<<<grid_for(cg.ncell, kListWarps), kListWarps * 32, 0, s>>>(
+            (const rec4*)q, (const rec4*)p, cg, start, atoms, perm, (rec4*)q_out, (rec4*)p_out, (rec4*)q_ref,
+            (rec4*)(ws + W.off_qcell), (float4*)(ws + W.off_qr), cg.L / cg.nc);
         g_launches += 2;
     }
     return cudaGetLastError();

@@ -21,7 +21,8 @@ LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 192   # include/liblj.h
 
 # every symbol include/liblj.h declares
 EXPORTS = (
-    "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_cell_order",
+    "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_rebuild",
+    "lj_cell_order",
     "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_gather_probe", "lj_integrate", "lj_wrap",
     "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
     "lj_version",
@@ -62,6 +63,8 @@ def load() -> ctypes.CDLL:
         "lj_build_list": (st, [vp, i64, Geom, i32, i64, i64, vp, vp, vp, i64, ctypes.POINTER(i64), vp, sz, vp]),
         "lj_build_list_ex": (st, [vp, i64, Geom, i32, i64, i64, i32, vp, vp, vp, i64, ctypes.POINTER(i64), vp, sz,
                                   vp]),
+        "lj_rebuild": (st, [vp, vp, vp, vp, vp, vp, i64, Geom, i32, i64, i64, i32, vp, vp, vp, i64,
+                            ctypes.POINTER(i64), vp, sz, vp]),
         "lj_cell_order": (st, [vp, i64, Geom, vp, vp, sz, vp]),
         "lj_permute_rows": (st, [vp, vp, vp, i64, vp]),
         "lj_force_step": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, vp]),
@@ -180,14 +183,30 @@ class ListBuilder:
 
     def build(self, q: torch.Tensor) -> CSRList:
         _rec(q, "q")
-        L = load()
+        return self._build(lambda ne: load().lj_build_list_ex(
+            _ptr(q), self.n, self.g, int(self.half), self.row_begin, self.row_end,
+            LJ_LIST_PADDED if self.padded else 0, _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
+            self.sorted_list.numel(), ctypes.byref(ne), _ptr(self.workspace), self.workspace.numel(), _stream()))
+
+    def rebuild(self, q: torch.Tensor, p: torch.Tensor | None, q_out: torch.Tensor, p_out: torch.Tensor | None,
+                q_ref: torch.Tensor | None, perm: torch.Tensor) -> CSRList:
+        """lj_rebuild: wrap q in place, permute (q, p) into cell order (q_out, p_out, q_ref = q_out,
+        perm[new] = old) and build the list of the permuted system, from one cell pass."""
+        for t, name in ((q, "q"), (q_out, "q_out"), (p, "p"), (p_out, "p_out"), (q_ref, "q_ref")):
+            if t is not None:
+                _rec(t, name)
+        if not (perm.is_cuda and perm.dtype == torch.int64 and perm.numel() == self.n):
+            raise TypeError("rebuild: perm must be a CUDA int64 tensor of length n")
+        return self._build(lambda ne: load().lj_rebuild(
+            _ptr(q), _ptr(p), _ptr(q_out), _ptr(p_out), _ptr(q_ref), _ptr(perm), self.n, self.g, int(self.half),
+            self.row_begin, self.row_end, LJ_LIST_PADDED if self.padded else 0, _ptr(self.npart),
+            _ptr(self.pointer), _ptr(self.sorted_list), self.sorted_list.numel(), ctypes.byref(ne),
+            _ptr(self.workspace), self.workspace.numel(), _stream()))
+
+    def _build(self, call) -> CSRList:
         ne = ctypes.c_int64(0)
         for _ in range(3):
-            st = L.lj_build_list_ex(_ptr(q), self.n, self.g, int(self.half), self.row_begin, self.row_end,
-                                    LJ_LIST_PADDED if self.padded else 0,
-                                    _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
-                                    self.sorted_list.numel(), ctypes.byref(ne), _ptr(self.workspace),
-                                    self.workspace.numel(), _stream())
+            st = call(ne)
             if st == LJ_ERR_UNSUPPORTED and self.padded:   # a row longer than the stride: compact from now on
                 self.padded = False
                 continue

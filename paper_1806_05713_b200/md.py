@@ -55,6 +55,12 @@ class LibBackend:
     def build(self, q):
         return self.builder.build(q)
 
+    def rebuild(self, q, p, q_out, p_out, q_ref):
+        """Fused wrap + cell-order permutation + list build (lj_rebuild, one cell pass)."""
+        if not hasattr(self, "perm"):
+            self.perm = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        return self.builder.rebuild(q, p, q_out, p_out, q_ref, self.perm)
+
     def cell_order(self, q):
         """perm[new] = old (stable sort by cell id), using the builder's workspace."""
         perm = torch.empty(self.n, dtype=torch.int64, device=self.device)
@@ -166,6 +172,11 @@ class LeapfrogMD:
         if self.reorder:
             if self.collective:
                 self._allgather(self.p)          # momenta of all rows, to follow the permutation
+            if hasattr(self.be, "rebuild"):      # one fused library call (lj_rebuild)
+                self.lst = self.be.rebuild(self.q, self.p, self.q_alt, self.p_alt, self.q_ref)
+                self.q, self.q_alt = self.q_alt, self.q
+                self.p, self.p_alt = self.p_alt, self.p
+                return
             self.be.wrap(self.q, None)
             perm = self.be.cell_order(self.q)
             self.be.permute(self.q, perm, self.q_alt)

@@ -413,3 +413,45 @@ def test_padded_layout_falls_back_on_long_rows(lj, dev):
     gl = b.build(to_dev(q, dev))
     assert not b.padded
     assert_same_list(gl, oracle.list_cells(q, 9.9, 3.3, False))
+
+
+@pytest.mark.parametrize("padded,rows", [(True, (0, 4000)), (False, (0, 4000)), (True, (1000, 3000)),
+                                         (False, (123, 456))])
+def test_rebuild_fused_equals_steps(lj, dev, systems, padded, rows):
+    """lj_rebuild == lj_wrap + lj_cell_order + lj_permute_rows (q, p, q_ref) +
+    lj_build_list_ex on the permuted system, bit for bit, for drifted (unwrapped)
+    positions; and its cell order equals the oracle's."""
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    rng = np.random.default_rng(41)
+    q_np = w.q + rng.uniform(-0.15, 0.15, w.q.shape)   # some atoms outside [0, L)
+    p_np = rng.normal(0, 1, (w.n, 3))
+    pad = np.arange(w.n, dtype=np.float64)
+    rb, re_ = rows
+    # step by step
+    qa = to_dev(q_np, dev, pad)
+    pa = to_dev(p_np, dev, pad)
+    lj.wrap(qa, w.L)
+    perm_a = lj.cell_order(qa, g)
+    qa2, pa2 = lj.permute_rows(qa, perm_a), lj.permute_rows(pa, perm_a)
+    la = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=padded).build(qa2)
+    # fused
+    qb = to_dev(q_np, dev, pad)
+    pb = to_dev(p_np, dev, pad)
+    qb2, pb2, qref = torch.empty_like(qb), torch.empty_like(pb), torch.empty_like(qb)
+    perm_b = torch.empty(w.n, dtype=torch.int64, device=dev)
+    lb = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=padded).rebuild(qb, pb, qb2, pb2, qref, perm_b)
+    assert torch.equal(qa, qb)          # wrapped in place
+    assert torch.equal(perm_a, perm_b)
+    assert torch.equal(qa2, qb2) and torch.equal(pa2, pb2) and torch.equal(qa2, qref)
+    assert la.n_entries == lb.n_entries
+    assert torch.equal(la.number_of_partners, lb.number_of_partners) and torch.equal(la.pointer, lb.pointer)
+    nrow = re_ - rb
+    for r in range(0, nrow, max(1, nrow // 50)):   # valid entries of sampled rows (padded rows have gaps)
+        b0, n0 = int(la.pointer[r]), int(la.number_of_partners[r])
+        assert torch.equal(la.sorted_list[b0:b0 + n0], lb.sorted_list[b0:b0 + n0])
+    # the permutation is the oracle's cell order of the wrapped positions
+    assert np.array_equal(perm_b.cpu().numpy(), oracle.cell_order(oracle.wrap(q_np, w.L), w.L, w.rs))
+    # and the list is the oracle's list of the permuted system
+    ol = oracle.list_cells(from_dev(qb2), w.L, w.rs, False, rb, re_)
+    assert int(lb.n_entries) == ol.n_entries
