@@ -275,6 +275,8 @@ def gather_probe(q: torch.Tensor, lst: CSRList, lanes_per_row: int = 0, sink: to
     _rec(q, "q")
     if sink is None:
         sink = torch.zeros(1, dtype=torch.float64, device=q.device)
+    if lanes_per_row == 0 and lst.padded:
+        lanes_per_row = 8   # the lanes force_step uses on padded lists
     _check(load().lj_gather_probe(_ptr(q), q.shape[0], lst.row_begin, lst.row_end, _ptr(lst.number_of_partners),
                                   _ptr(lst.pointer), _ptr(lst.sorted_list), int(lanes_per_row), _ptr(sink),
                                   _stream()))
