@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--order", default=None, choices=["lattice", "shuffled", "cell"],
                     help="storage order; default: config 2 shuffled, 3 cell, 4/5 cell (re-sorted at every rebuild)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true", help="P > 1: blocking all-gather (no comm/compute overlap)")
     ap.add_argument("--energy-every", type=int, default=None,
                     help="NVE energy sample interval in timed steps (default: config 5 -> steps/20, else off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -219,7 +220,8 @@ def main():
     order = args.order or {2: "shuffled", 3: "cell"}.get(args.config, "cell")
     rb, re_ = md.row_range(w.n, rank, world)
     be = md.LibBackend(w.n, g, rb, re_, dev, half=half)
-    sim = md.LeapfrogMD(be, w.q, w.p, g, w.dt, rank, world, comm, reorder=(order == "cell"))
+    sim = md.LeapfrogMD(be, w.q, w.p, g, w.dt, rank, world, comm, reorder=(order == "cell"),
+                        overlap=not args.no_overlap)
     if not force_only:
         sim.start_leapfrog()   # p_0 -> p_{-1/2}
 
@@ -235,19 +237,18 @@ def main():
             a.record(stream)
         e = None
         if sample:
+            sim.sync_positions()
             be.force(sim.q, sim.p, 0.5 * w.dt, sim.lst, sim.counter)
             e = sim.energy()
             be.force(sim.q, sim.p, 0.5 * w.dt, sim.lst)
         else:
-            be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
+            sim.kick(w.dt, sim.counter)   # interior rows overlap the pending all-gather (P > 1)
         if rec:
             b.record(stream)
             f_ev.append((a, b))
         if force_only:
             return e
-        be.integrate(sim.q, sim.p, w.dt, sim.rb, sim.re)
-        sim._allgather_q()
-        sim.check_rebuild()
+        sim.drift_and_exchange()          # integrate, displacement check, all-gather / rebuild
         return e
 
     every = args.energy_every if args.energy_every is not None else (max(1, args.steps // 20) if args.config == 5 else 0)
@@ -268,6 +269,7 @@ def main():
         e = one_step(True, sample=(every > 0 and not force_only and k % every == 0))
         if e is not None:
             energies.append((k, e[0], e[1]))
+    sim.sync_positions()
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -354,6 +356,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
+            sim.sync_positions()
             sim.q[rb:re_].copy_(qh, non_blocking=True)
             sim.p[rb:re_].copy_(ph, non_blocking=True)
             one_step(False)
@@ -390,6 +393,8 @@ def main():
             "config": {"workload": f"config{args.config}", "n_atoms": w.n, "list": "half" if half else "full",
                        "order": order + (" (re-sorted at every rebuild)" if order == "cell" and not force_only else ""),
                        "dt": w.dt, "rc": w.rc, "rs": w.rs, "parallelism": f"rows/{world}",
+                       "exchange": ("async all-gather overlapped with the interior rows' force" if sim.overlap
+                                    else ("all-gather" if world > 1 else "none (1 rank)")),
                        "l2": "inputs larger than L2 (CSR list %.2f GB + records)" % (4 * sim.lst.n_entries / 1e9),
                        "rebuilds_in_timed_steps": rebuilds},
             "ms_per_force_step": force_avg,

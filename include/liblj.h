@@ -13,9 +13,11 @@
  *    into arithmetic and is preserved by every call.
  *  - Lists are the paper's sorted list (Fig. sorted_list) in
  *    CSR form, local to a row range [row_begin, row_end): row r <-> atom
- *    row_begin + r; number_of_partners[rows] (int32), pointer[rows+1] (int64,
- *    pointer[0] = 0), sorted_list[pointer[rows]] (int32 global atom indices,
- *    ascending within a row).  n < 2^31 is checked.
+ *    row_begin + r; number_of_partners[rows] (int32), pointer[rows+1] (int64;
+ *    the builder writes pointer[0] = 0, consumers only read row r's entries at
+ *    sorted_list + pointer[r], so a contiguous sub-range of rows is addressed by
+ *    offsetting number_of_partners and pointer), sorted_list (int32 global atom
+ *    indices, ascending within a row).  n < 2^31 is checked.
  *  - Full list (half = 0): row i holds every j != i with r_ij^2 < rs^2.
  *    Half list (half = 1): row i holds only j > i (each pair once, PAPER.md
  *    Alg. calcforce_sortedlist); a half list must cover all rows [0, n).
@@ -161,6 +163,16 @@ lj_status lj_force_step_ex(const double *q, double *p, int64_t n, lj_geom g, dou
 lj_status lj_gather_probe(const double *q, int64_t n, int64_t row_begin, int64_t row_end,
                           const int32_t *number_of_partners, const int64_t *pointer,
                           const int32_t *sorted_list, int lanes_per_row, double *sink, void *stream);
+
+/* Interior rows of a row-split full list (comm/compute
+ * overlap): out (device, 2 x int64) = {A, B} such that every row in [A, B)
+ * has all its partners inside [row_begin, row_end) -- the force on those rows
+ * needs no position of another rank, so it can run while the all-gather of
+ * the other ranks' positions is in flight.  [A, B) is the contiguous interior
+ * run around the middle row (A = row_begin, B = row_end if no row looks
+ * outside).  Asynchronous. */
+lj_status lj_list_interior(int64_t row_begin, int64_t row_end, const int32_t *number_of_partners,
+                           const int64_t *pointer, const int32_t *sorted_list, int64_t *out, void *stream);
 
 /* ---- integration and bookkeeping (§8(a) a7, a9) --------------------------- */
 

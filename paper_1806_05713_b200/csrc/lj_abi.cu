@@ -341,6 +341,17 @@ lj_status lj_gather_probe(const double* q, int64_t n, int64_t row_begin, int64_t
     return LJ_OK;
 }
 
+lj_status lj_list_interior(int64_t row_begin, int64_t row_end, const int32_t* number_of_partners,
+                           const int64_t* pointer, const int32_t* sorted_list, int64_t* out, void* stream) {
+    if (row_begin < 0 || row_end < row_begin) return fail(LJ_ERR_ARG, "list_interior: bad row range");
+    if (!out || (row_end > row_begin && (!number_of_partners || !pointer || !sorted_list)))
+        return fail(LJ_ERR_ARG, "list_interior: null pointer");
+    LJ_CUDA(launch_list_interior(row_begin, row_end, number_of_partners, pointer, sorted_list, out,
+                                 (cudaStream_t)stream),
+            "lj_list_interior");
+    return LJ_OK;
+}
+
 lj_status lj_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, void* stream) {
     if (begin < 0 || end < begin || end > (int64_t)INT32_MAX)
         return fail(LJ_ERR_ARG, "integrate: bad range [%lld,%lld)", (long long)begin, (long long)end);

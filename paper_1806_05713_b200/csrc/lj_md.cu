@@ -140,7 +140,53 @@ __global__ void k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p,
     }
 }
 
+// Interior rows for comm/compute overlap: row r is
+// "boundary" if some partner lies outside [row_begin, row_end).  out[0] =
+// max{i < mid : boundary} (init row_begin - 1), out[1] = min{i >= mid :
+// boundary} (init row_end); [out[0] + 1, out[1]) is then the contiguous run of
+// interior rows around mid = (row_begin + row_end) / 2.  One warp per row.
+__global__ void k_list_interior(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ npart,
+                                const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
+                                unsigned long long* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t mid = (row_begin + row_end) / 2;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < row_end - row_begin;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int n = npart[r];
+        const int32_t* l = list + ptr[r];
+        bool out_of_slab = false;
+        for (int k = lane; k < n; k += 32) {
+            const int j = l[k];
+            out_of_slab |= j < row_begin || j >= row_end;
+        }
+        if (__any_sync(0xffffffffu, out_of_slab) && lane == 0) {
+            const int64_t i = row_begin + r;
+            if (i < mid)
+                atomicMax(&out[0], (unsigned long long)(i + 1));   // stored +1 so that "none" = row_begin
+            else
+                atomicMin(&out[1], (unsigned long long)i);
+        }
+    }
+}
+
+__global__ void k_init_interior(unsigned long long* out, int64_t row_begin, int64_t row_end) {
+    out[0] = (unsigned long long)row_begin;
+    out[1] = (unsigned long long)row_end;
+}
+
 }  // namespace
+
+cudaError_t launch_list_interior(int64_t row_begin, int64_t row_end, const int32_t* npart, const int64_t* ptr,
+                                 const int32_t* list, int64_t* out, cudaStream_t s) {
+    k_init_interior<<<1, 1, 0, s>>>((unsigned long long*)out, row_begin, row_end);
+    g_launches++;
+    if (row_end > row_begin) {
+        k_list_interior<<<grid_for((row_end - row_begin) * 32, kThreads, 148 * 16), kThreads, 0, s>>>(
+            row_begin, row_end, npart, ptr, list, (unsigned long long*)out);
+        g_launches++;
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pack(const double* xyz, double* out, int64_t n, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

@@ -23,7 +23,8 @@ LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 192   # include/liblj.h
 EXPORTS = (
     "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_rebuild",
     "lj_cell_order",
-    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_gather_probe", "lj_integrate", "lj_wrap",
+    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_gather_probe", "lj_list_interior", "lj_integrate",
+    "lj_wrap",
     "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
     "lj_version",
 )
@@ -70,6 +71,7 @@ def load() -> ctypes.CDLL:
         "lj_force_step": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, vp]),
         "lj_force_step_ex": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, i32, i32, vp, vp]),
         "lj_gather_probe": (st, [vp, i64, i64, i64, vp, vp, vp, i32, vp, vp]),
+        "lj_list_interior": (st, [i64, i64, vp, vp, vp, vp, vp]),
         "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
         "lj_wrap": (st, [vp, vp, i64, d, vp]),
         "lj_max_displacement": (st, [vp, vp, i64, i64, vp, vp]),
@@ -157,6 +159,15 @@ class CSRList:
     @property
     def rows(self):
         return self.row_end - self.row_begin
+
+    def rows_view(self, a: int, b: int) -> "CSRList":
+        """The rows [a, b) (global indices, within this list's range) as a list of
+        their own: offset views of number_of_partners and pointer, same entries."""
+        if not (self.row_begin <= a <= b <= self.row_end):
+            raise ValueError(f"rows_view: [{a},{b}) not within [{self.row_begin},{self.row_end})")
+        o = a - self.row_begin
+        return CSRList(self.number_of_partners[o:o + (b - a)], self.pointer[o:], self.sorted_list, self.n_entries,
+                       a, b, self.half, self.padded)
 
 
 class ListBuilder:
@@ -280,6 +291,16 @@ def gather_probe(q: torch.Tensor, lst: CSRList, lanes_per_row: int = 0, sink: to
     _check(load().lj_gather_probe(_ptr(q), q.shape[0], lst.row_begin, lst.row_end, _ptr(lst.number_of_partners),
                                   _ptr(lst.pointer), _ptr(lst.sorted_list), int(lanes_per_row), _ptr(sink),
                                   _stream()))
+
+
+def list_interior(lst: CSRList) -> tuple[int, int]:
+    """(A, B): rows [A, B) of the list's range have all partners inside the range
+    (lj_list_interior; one 16-byte readback)."""
+    out = torch.empty(2, dtype=torch.int64, device=lst.pointer.device)
+    _check(load().lj_list_interior(lst.row_begin, lst.row_end, _ptr(lst.number_of_partners), _ptr(lst.pointer),
+                                   _ptr(lst.sorted_list), _ptr(out), _stream()))
+    a, b = out.tolist()
+    return int(a), int(b)
 
 
 def integrate(q: torch.Tensor, p: torch.Tensor, dt: float, begin: int = 0, end: int | None = None) -> None:

@@ -9,12 +9,14 @@ of its own rows.  Per step (SURVEY §3 call stack 4):
 
     force(dt) on own rows          -- liblj lj_force_step (kernel)
     integrate(dt) on own rows      -- liblj lj_integrate (kernel)
-    all-gather q                   -- torch.distributed (NCCL), P > 1 only
     disp = max |q - q_ref| own     -- liblj lj_max_displacement (kernel)
     all-reduce MAX disp            -- torch.distributed, P > 1 only
     if 2 disp >= rs - rc:          -- host decision (one 8-byte readback)
-        wrap q, q_ref <- q         -- liblj lj_wrap (kernel)
-        rebuild own rows           -- liblj lj_build_list (kernels)
+        all-gather q; rebuild      -- lj_rebuild (wrap + cell order + list)
+    else: all-gather q             -- NCCL, P > 1 only; asynchronous with
+                                      overlap: the next force step computes the
+                                      interior rows (partners all own,
+                                      lj_list_interior) while it is in flight
 
 The compute backend is injectable so the multi-rank plumbing can be tested on
 CPU with gloo (tests/test_dist_gloo.py); the product backend is LibBackend,
@@ -75,6 +77,14 @@ class LibBackend:
     def force(self, q, p, dt, lst, counter=None):
         lj.force_step(q, p, self.g, dt, lst, n_interactions=counter)
 
+    def force_rows(self, q, p, dt, lst, a, b, counter=None):
+        """Force on the rows [a, b) of lst only."""
+        lj.force_step(q, p, self.g, dt, lst.rows_view(a, b), n_interactions=counter)
+
+    def interior(self, lst):
+        """Rows [A, B) whose partners are all own rows (lj_list_interior)."""
+        return lj.list_interior(lst)
+
     def integrate(self, q, p, dt, b, e):
         lj.integrate(q, p, dt, b, e)
 
@@ -99,7 +109,7 @@ class LeapfrogMD:
     torch.distributed process group (NCCL on GPUs, gloo in CPU tests)."""
 
     def __init__(self, backend, q_xyz, p_xyz, g: lj.Geom, dt: float, rank: int = 0, world: int = 1, comm=None,
-                 count_interactions: bool = True, reorder: bool = True):
+                 count_interactions: bool = True, reorder: bool = True, overlap: bool | None = None):
         self.be, self.g, self.dt = backend, g, float(dt)
         self.n = q_xyz.shape[0]
         self.rank, self.world, self.comm = rank, world, comm
@@ -121,6 +131,13 @@ class LeapfrogMD:
         if reorder:
             self.q_alt = backend.empty_records(self.n)
             self.p_alt = backend.empty_records(self.n)
+        # comm/compute overlap: the all-gather of the positions
+        # runs asynchronously while the next force step computes the interior rows
+        # (all partners own); boundary rows wait for it.  Needs equal slabs.
+        can = self.collective and self.n % world == 0 and hasattr(backend, "force_rows")
+        self.overlap = can if overlap is None else (bool(overlap) and can)
+        self._pending = None                  # async all-gather of q in flight
+        self.interior_rows = (self.rb, self.re)
         self._rebuild()
 
     # ---- collectives (no-ops for one rank) ----
@@ -144,7 +161,21 @@ class LeapfrogMD:
                         x[b:e] = buf[r * m: r * m + (e - b)]
 
     def _allgather_q(self):
+        self.sync_positions()
         self._allgather(self.q)
+
+    def _allgather_q_async(self):
+        """Start the in-place all-gather of the own position rows (completed by sync_positions)."""
+        if self.collective:
+            own = self.q[self.rb:self.re]
+            self._pending = dist.all_gather_into_tensor(self.q, own.clone() if self._gloo() else own,
+                                                        group=self.comm, async_op=True)
+
+    def sync_positions(self):
+        """Complete a pending all-gather: afterwards every rank's q holds all positions."""
+        if self._pending is not None:
+            self._pending.wait()
+            self._pending = None
 
     def _gloo(self):
         return dist.get_backend(self.comm) == "gloo"
@@ -160,6 +191,7 @@ class LeapfrogMD:
     # ---- MD ----
     def half_kick(self, sign: float = 1.0):
         """p += sign F(q) dt/2."""
+        self.sync_positions()
         self.be.force(self.q, self.p, sign * 0.5 * self.dt, self.lst)
 
     def start_leapfrog(self):
@@ -169,6 +201,12 @@ class LeapfrogMD:
     def _rebuild(self):
         """Wrap, (optionally) re-sort the atoms into cell order (§8(a) a3), snapshot
         q_ref and rebuild the own-row list (§8(a) a2-a4)."""
+        self.sync_positions()
+        self._rebuild_lists()
+        if self.overlap:
+            self.interior_rows = self.be.interior(self.lst)
+
+    def _rebuild_lists(self):
         if self.reorder:
             if self.collective:
                 self._allgather(self.p)          # momenta of all rows, to follow the permutation
@@ -199,6 +237,38 @@ class LeapfrogMD:
             return True
         return False
 
+    def kick(self, dt: float, counter=None):
+        """p += F(q) dt on own rows.  With an all-gather in flight, the interior
+        rows go first (they read own positions only), then the boundary rows
+        once the other ranks' positions have arrived."""
+        if self._pending is None:
+            self.be.force(self.q, self.p, dt, self.lst, counter)
+            return
+        a, b = self.interior_rows
+        if b > a:
+            self.be.force_rows(self.q, self.p, dt, self.lst, a, b, counter)
+        self.sync_positions()
+        if a > self.rb:
+            self.be.force_rows(self.q, self.p, dt, self.lst, self.rb, a, counter)
+        if self.re > b:
+            self.be.force_rows(self.q, self.p, dt, self.lst, b, self.re, counter)
+
+    def drift_and_exchange(self):
+        """q += p dt on own rows, the bookkeeping check (displacement all-reduce
+        MAX first), then the position exchange: a blocking all-gather + rebuild
+        when the list expires, else the all-gather (asynchronous with overlap)."""
+        self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
+        self.be.max_disp(self.q, self.q_ref, self.rb, self.re, self.disp)
+        self._allreduce_max(self.disp)
+        if 2.0 * float(self.disp.item()) >= self.margin:
+            self._allgather_q()
+            self._rebuild()
+            self.stats.rebuilds += 1
+        elif self.overlap:
+            self._allgather_q_async()
+        else:
+            self._allgather_q()
+
     def step(self, sample: bool = False):
         """One leapfrog step: p += F(q) dt; q += p dt; all-gather; bookkeeping.
         With sample=True the kick is split in two halves around an energy
@@ -206,19 +276,19 @@ class LeapfrogMD:
         (reading O8/C-17); returns (KE, PE) then, else None."""
         e = None
         if sample:
+            self.sync_positions()
             self.be.force(self.q, self.p, 0.5 * self.dt, self.lst, self.counter)
             e = self.energy()
             self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
         else:
-            self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
-        self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
-        self._allgather_q()
-        self.check_rebuild()
+            self.kick(self.dt, self.counter)
+        self.drift_and_exchange()
         self.stats.steps += 1
         return e
 
     def kdk_step(self):
         """One synchronised velocity-Verlet step (O8): kick dt/2, drift, rebuild check, kick dt/2."""
+        self.sync_positions()
         self.be.force(self.q, self.p, 0.5 * self.dt, self.lst)
         self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
         self._allgather_q()
@@ -228,6 +298,7 @@ class LeapfrogMD:
 
     def energy(self):
         """(KE, PE) summed over ranks (p must be synchronised, e.g. after kdk_step)."""
+        self.sync_positions()
         out = torch.zeros(2, dtype=torch.float64, device=self.q.device)
         self.be.energy(self.q, self.p, self.lst, out)
         self._allreduce_sum(out)

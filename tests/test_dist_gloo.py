@@ -50,6 +50,27 @@ class OracleBackend:
         out = oracle.force_step(self._xyz(q), self._xyz(p), self.g.L, self.g.rc, dt, lst)
         p[:, :3] = torch.as_tensor(out)
 
+    def force_rows(self, q, p, dt, lst, a, b, counter=None):
+        o = a - lst.row_begin
+        sub = oracle.CSR(lst.number_of_partners[o:o + (b - a)], lst.pointer[o:o + (b - a) + 1], lst.sorted_list,
+                         a, b, lst.half)
+        self.force(q, p, dt, sub)
+
+    def interior(self, lst):
+        """Same definition as lj_list_interior, in numpy."""
+        rb, re_ = lst.row_begin, lst.row_end
+        mid = (rb + re_) // 2
+        a, b = rb, re_
+        for r in range(lst.rows):
+            j = lst.row(r)
+            if len(j) and (j.min() < rb or j.max() >= re_):
+                i = rb + r
+                if i < mid:
+                    a = max(a, i + 1)
+                else:
+                    b = min(b, i)
+        return a, b
+
     def integrate(self, q, p, dt, b, e):
         q[:, :3] = torch.as_tensor(oracle.integrate(self._xyz(q), self._xyz(p), dt, b, e))
 
@@ -66,20 +87,25 @@ class OracleBackend:
         out[0], out[1] = ke, pe
 
 
-def make_system(n_drop):
-    w = lj_inputs.make_system(8, jitter_seed=1, T=1.0, mom_seed=5, dt=0.01)
+def make_system(n_drop, cells=8):
+    w = lj_inputs.make_system(cells, jitter_seed=1, T=1.0, mom_seed=5, dt=0.01)
     q, p = w.q, w.p
     if n_drop:
         q, p = q[:-n_drop].copy(), p[:-n_drop].copy()
     return w, q, p
 
 
-def run(rank, world, n_drop, reorder, steps, comm=None):
-    w, q, p = make_system(n_drop)
+def run(rank, world, n_drop, reorder, steps, comm=None, overlap=None):
+    # overlap needs slabs wider than 2 r_s to have interior rows: 12^3 FCC cells (L = 19)
+    w, q, p = make_system(n_drop, 12 if overlap else 8)
     g = lj.geom(w.L, w.rc, w.rs)
     rb, re_ = md.row_range(q.shape[0], rank, world)
     sim = md.LeapfrogMD(OracleBackend(q.shape[0], g, rb, re_), q, p, g, w.dt, rank, world, comm,
-                        count_interactions=False, reorder=reorder)
+                        count_interactions=False, reorder=reorder, overlap=overlap)
+    if world > 1 and overlap:
+        assert sim.overlap
+        a, b = sim.interior_rows
+        assert rb < a < b < re_, "the slabs must have interior and boundary rows"
     sim.half_kick()
     for _ in range(steps):
         sim.step()
@@ -91,12 +117,12 @@ def run(rank, world, n_drop, reorder, steps, comm=None):
     return sim.q.numpy().copy(), p_full.numpy().copy(), sim.stats.rebuilds, e
 
 
-def _worker(rank, world, port, n_drop, reorder, steps, outdir):
+def _worker(rank, world, port, n_drop, reorder, steps, outdir, overlap=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        q, p, rb, e = run(rank, world, n_drop, reorder, steps, dist.group.WORLD)
+        q, p, rb, e = run(rank, world, n_drop, reorder, steps, dist.group.WORLD, overlap)
         np.savez(os.path.join(outdir, f"r{rank}.npz"), q=q, p=p, rb=rb, e=np.array(e))
     finally:
         dist.destroy_process_group()
@@ -110,12 +136,15 @@ def free_port():
     return port
 
 
-@pytest.mark.parametrize("n_drop,reorder", [(0, True), (0, False), (3, True)])
-def test_two_ranks_equal_one_rank(tmp_path, n_drop, reorder):
+@pytest.mark.parametrize("n_drop,reorder,overlap", [(0, True, False), (0, False, False), (3, True, None),
+                                                    (0, True, True), (0, False, True)])
+def test_two_ranks_equal_one_rank(tmp_path, n_drop, reorder, overlap):
+    """overlap=True: the all-gather runs asynchronously while the interior rows'
+    forces are computed -- still bit-identical."""
     steps = 12        # T = 1, dt = 0.01: the list is rebuilt every ~4-5 steps
-    q1, p1, rb1, e1 = run(0, 1, n_drop, reorder, steps)
+    q1, p1, rb1, e1 = run(0, 1, n_drop, reorder, steps, overlap=overlap)
     assert rb1 >= 2, "the test must exercise rebuilds"
-    mp.start_processes(_worker, args=(2, free_port(), n_drop, reorder, steps, str(tmp_path)), nprocs=2,
+    mp.start_processes(_worker, args=(2, free_port(), n_drop, reorder, steps, str(tmp_path), overlap), nprocs=2,
                        start_method="spawn")
     for r in range(2):
         d = np.load(tmp_path / f"r{r}.npz")

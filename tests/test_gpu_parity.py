@@ -455,3 +455,35 @@ def test_rebuild_fused_equals_steps(lj, dev, systems, padded, rows):
     # and the list is the oracle's list of the permuted system
     ol = oracle.list_cells(from_dev(qb2), w.L, w.rs, False, rb, re_)
     assert int(lb.n_entries) == ol.n_entries
+
+
+@pytest.mark.parametrize("rows", [(0, 4000), (1000, 3000), (1500, 1800)])
+def test_list_interior_and_row_views(lj, dev, systems, rows):
+    """lj_list_interior against its definition (numpy over the oracle's list), and
+    the force over row views [rb,A) + [A,B) + [B,re) == the force over [rb,re),
+    bit for bit (full-list rows are independent)."""
+    w = systems[3]   # cell order: the slab's boundary rows sit at its ends
+    g = lj.geom(w.L, w.rc, w.rs)
+    rb, re_ = rows
+    q = to_dev(w.q, dev)
+    gl = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=True).build(q)
+    A, B = lj.list_interior(gl)
+    ol = oracle.list_cells(w.q, w.L, w.rs, False, rb, re_)
+    mid = (rb + re_) // 2
+    a, b = rb, re_
+    for r in range(ol.rows):
+        j = ol.row(r)
+        if len(j) and (j.min() < rb or j.max() >= re_):
+            i = rb + r
+            if i < mid:
+                a = max(a, i + 1)
+            else:
+                b = min(b, i)
+    assert (A, B) == (a, b)
+    p0 = np.random.default_rng(51).normal(0, 1, (w.n, 3))
+    pa, pb = to_dev(p0, dev), to_dev(p0, dev)
+    lj.force_step(q, pa, g, w.dt, gl)
+    for x, y in ((A, B), (rb, A), (B, re_)):
+        if y > x:
+            lj.force_step(q, pb, g, w.dt, gl.rows_view(x, y))
+    assert torch.equal(pa, pb)
