@@ -155,6 +155,31 @@ lj_status lj_force_step_ex(const double *q, double *p, int64_t n, lj_geom g, dou
                            const int32_t *sorted_list, int lanes_per_row, int ordered,
                            unsigned long long *n_interactions, void *stream);
 
+/* ---- paper-variant ablations (not the hot path) ------- */
+
+/* Position/momentum layouts of the paper's variant axis (PAPER.md:117-126,
+ * 341-353, 551-573).  q and p are n atoms in the given layout (for AOS8 both
+ * live in q's 64-byte records and p is ignored). */
+#define LJ_LAYOUT_AOS4 0   /* x, y, z, pad: 32-B records (the library's layout) */
+#define LJ_LAYOUT_SOA 1    /* x[n], y[n], z[n]: 3n doubles, x block first */
+#define LJ_LAYOUT_AOS3 2   /* x, y, z without padding: 24-B records */
+#define LJ_LAYOUT_AOS8 3   /* q.x, q.y, q.z, pad, p.x, p.y, p.z, pad: 64-B records */
+/* 1/r^2 evaluation (the paper's reciprocal "future issue"). */
+#define LJ_RCP_NEWTON3 0   /* rcp.approx + one cubic Newton step (lj_force_step) */
+#define LJ_RCP_NEWTON2 1   /* rcp.approx + one quadratic Newton step */
+#define LJ_RCP_APPROX 2    /* rcp.approx (MUFU.RCP64H) alone */
+#define LJ_RCP_IEEE 3      /* correctly rounded reciprocal */
+
+/* lj_force_step (full list only) in another layout / reciprocal: the same
+ * lanes-per-row kernel structure and arithmetic as lj_force_step, only the
+ * gathers, the momentum commit or 1/r^2 differ (so LJ_LAYOUT_* with
+ * LJ_RCP_NEWTON3 give bit-identical momenta).  lanes_per_row: 4 or 8.
+ * Alignment: 32 B for AOS4/AOS8, 8 B otherwise. */
+lj_status lj_force_step_variant(int layout, int rcp, const double *q, double *p, int64_t n, lj_geom g, double dt,
+                                int64_t row_begin, int64_t row_end, const int32_t *number_of_partners,
+                                const int64_t *pointer, const int32_t *sorted_list, int lanes_per_row,
+                                unsigned long long *n_interactions, void *stream);
+
 /* Roofline probe (not part of the method): the memory traffic of lj_force_step
  * on a full list -- the same lanes-per-row mapping, index loads and 256-bit
  * record gathers -- with no arithmetic beyond a running sum written to *sink

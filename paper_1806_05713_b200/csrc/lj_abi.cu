@@ -314,6 +314,39 @@ lj_status lj_force_step(const double* q, double* p, int64_t n, lj_geom g, double
                             nullptr, stream);
 }
 
+lj_status lj_force_step_variant(int layout, int rcp, const double* q, double* p, int64_t n, lj_geom g, double dt,
+                                int64_t row_begin, int64_t row_end, const int32_t* number_of_partners,
+                                const int64_t* pointer, const int32_t* sorted_list, int lanes_per_row,
+                                unsigned long long* n_interactions, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, false));
+    LJ_TRY(check_rows(n, row_begin, row_end));
+    if (layout < LJ_LAYOUT_AOS4 || layout > LJ_LAYOUT_AOS8) return fail(LJ_ERR_ARG, "variant: unknown layout %d", layout);
+    if (rcp < LJ_RCP_NEWTON3 || rcp > LJ_RCP_IEEE) return fail(LJ_ERR_ARG, "variant: unknown reciprocal %d", rcp);
+    if (lanes_per_row != 4 && lanes_per_row != 8) return fail(LJ_ERR_ARG, "variant: lanes_per_row must be 4 or 8");
+    if (!std::isfinite(dt)) return fail(LJ_ERR_ARG, "variant: dt not finite");
+    const int64_t rows = row_end - row_begin;
+    if (layout == LJ_LAYOUT_AOS8) p = const_cast<double*>(q);
+    if (rows > 0 && (!q || !p || !number_of_partners || !pointer)) return fail(LJ_ERR_ARG, "variant: null pointer");
+    const bool wide = layout == LJ_LAYOUT_AOS4 || layout == LJ_LAYOUT_AOS8;
+    if (wide ? (!aligned32(q) || !aligned32(p)) : (((uintptr_t)q | (uintptr_t)p) & 7u))
+        return fail(LJ_ERR_ARG, "variant: q/p misaligned for the layout");
+    ForceArgs a;
+    a.q = q;
+    a.p = p;
+    a.row_begin = row_begin;
+    a.rows = rows;
+    a.npart = number_of_partners;
+    a.ptr = pointer;
+    a.list = sorted_list;
+    a.L = g.L;
+    a.rc2 = g.rc * g.rc;
+    a.dt = dt;
+    a.n_inter = n_interactions;
+    LJ_CUDA(launch_force_variant(a, n, layout, rcp, lanes_per_row, (cudaStream_t)stream), "lj_force_step_variant");
+    return LJ_OK;
+}
+
 lj_status lj_gather_probe(const double* q, int64_t n, int64_t row_begin, int64_t row_end,
                           const int32_t* number_of_partners, const int64_t* pointer, const int32_t* sorted_list,
                           int lanes_per_row, double* sink, void* stream) {

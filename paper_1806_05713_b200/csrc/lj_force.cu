@@ -182,6 +182,131 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : 3)
     count_interactions(cnt, n_inter);
 }
 
+// ---- paper-variant ablations -------------------------
+// The paper's layout axis (SoA vs AoS with padding, AoS8
+// P:551-573) and its reciprocal "future issue" on the GPU: the
+// full-list kernel of k_force (same lanes, same chunk loop and arithmetic)
+// with the position gather / momentum commit of another layout, and the 1/r^2
+// evaluated four ways.  Not on the hot path; lj_force_step_variant.
+template <int LAYOUT>
+struct Layout;
+template <>
+struct Layout<LJ_LAYOUT_AOS4> {   // x, y, z, pad: one 256-bit load
+    __device__ static void pos(const double* q, int64_t, int64_t j, double& x, double& y, double& z) {
+        const rec4 r = load_rec((const rec4*)q, j);
+        x = r.x, y = r.y, z = r.z;
+    }
+    __device__ static double* mom(double* p, int64_t, int64_t i, int c) { return p + 4 * i + c; }
+};
+template <>
+struct Layout<LJ_LAYOUT_SOA> {    // x[n], y[n], z[n]: three 8-byte gathers (three sectors)
+    __device__ static void pos(const double* q, int64_t n, int64_t j, double& x, double& y, double& z) {
+        x = __ldg(q + j), y = __ldg(q + n + j), z = __ldg(q + 2 * n + j);
+    }
+    __device__ static double* mom(double* p, int64_t n, int64_t i, int c) { return p + c * n + i; }
+};
+template <>
+struct Layout<LJ_LAYOUT_AOS3> {   // x, y, z without padding: 24-B records, three 8-byte loads
+    __device__ static void pos(const double* q, int64_t, int64_t j, double& x, double& y, double& z) {
+        x = __ldg(q + 3 * j), y = __ldg(q + 3 * j + 1), z = __ldg(q + 3 * j + 2);
+    }
+    __device__ static double* mom(double* p, int64_t, int64_t i, int c) { return p + 3 * i + c; }
+};
+template <>
+struct Layout<LJ_LAYOUT_AOS8> {   // one 64-B record per atom: q (x, y, z, pad) then p (x, y, z, pad)
+    __device__ static void pos(const double* q, int64_t, int64_t j, double& x, double& y, double& z) {
+        const rec4 r = load_rec((const rec4*)q, 2 * j);
+        x = r.x, y = r.y, z = r.z;
+    }
+    __device__ static double* mom(double* p, int64_t, int64_t i, int c) { return p + 8 * i + 4 + c; }
+};
+
+template <int RCP>
+__device__ __forceinline__ double inv_r2(double x) {
+    if (RCP == LJ_RCP_NEWTON3) return fast_rcp(x);
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    if (RCP == LJ_RCP_NEWTON2) return fma(y, fma(-x, y, 1.0), y);   // one quadratic Newton step
+    if (RCP == LJ_RCP_APPROX) return y;                              // MUFU.RCP64H alone
+    return __drcp_rn(x);                                             // IEEE reciprocal
+}
+
+// 48 registers (5 CTAs/SM, as k_force) where it does not spill; the 8-byte-gather
+// layouts need 64 (4 CTAs/SM).
+template <int G, int LAYOUT, int RCP>
+__global__ void __launch_bounds__(kForceThreads, (LAYOUT == LJ_LAYOUT_SOA || LAYOUT == LJ_LAYOUT_AOS3) ? 4 : 5)
+    k_force_variant(const double* __restrict__ q, double* __restrict__ p, int64_t n_atoms, int64_t row_begin,
+                    int64_t rows, const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr,
+                    const int32_t* __restrict__ list, PairConsts c, unsigned long long* n_inter) {
+    constexpr int U = 2;
+    using Lay = Layout<LAYOUT>;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    const bool active = r < rows;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    unsigned cnt = 0;
+    const int64_t i = row_begin + (active ? r : 0);
+    double qix, qiy, qiz;
+    Lay::pos(q, n_atoms, active ? i : 0, qix, qiy, qiz);
+    const int32_t* __restrict__ lst = list + (active ? ptr[r] : 0);
+    const int n = active ? npart[r] : 0;
+    int jn[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
+    for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
+        int j[U];
+        double dx[U], dy[U], dz[U], r2[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            j[u] = jn[u];
+            Lay::pos(q, n_atoms, j[u] >= 0 ? (int64_t)j[u] : i, dx[u], dy[u], dz[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int kn = k0 + U * G + u * G;
+            jn[u] = kn < n ? __ldg(lst + kn) : -1;
+        }
+        int hmax = 0;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            dx[u] -= qix;
+            dy[u] -= qiy;
+            dz[u] -= qiz;
+            r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+            hmax = max(hmax, __double2hiint(r2[u]));
+        }
+        if (__any_sync(0xffffffffu, hmax >= c.hi_L2q)) {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                dx[u] -= image_shift(dx[u], c.L, c.hi_halfL);
+                dy[u] -= image_shift(dy[u], c.L, c.hi_halfL);
+                dz[u] -= image_shift(dz[u], c.L, c.hi_halfL);
+                r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const double inv2 = inv_r2<RCP>(r2[u]);
+            const double inv6 = inv2 * inv2 * inv2;
+            const bool in = j[u] >= 0 && __double_as_longlong(r2[u]) < c.rc2_bits;
+            const double df = in ? fma(c.c48, inv6, -c.c24) * (inv6 * inv2) : 0.0;
+            ax = fma(-df, dx[u], ax);
+            ay = fma(-df, dy[u], ay);
+            az = fma(-df, dz[u], az);
+            cnt += in;
+        }
+    }
+    unsigned cnt_row = cnt;
+    group_reduce<G>(ax, ay, az, cnt_row);
+    if (active && g == 0) {
+        *Lay::mom(p, n_atoms, i, 0) += ax;
+        *Lay::mom(p, n_atoms, i, 1) += ay;
+        *Lay::mom(p, n_atoms, i, 2) += az;
+    }
+    count_interactions(cnt, n_inter);
+}
+
 // Roofline probe: the force kernel's access pattern (G lanes per row, two
 // gathers in flight, next indices prefetched) without the arithmetic.
 template <int G>
@@ -332,6 +457,46 @@ cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cud
     }
     g_launches++;
     return cudaGetLastError();
+}
+
+template <int G, int LAYOUT>
+static cudaError_t launch_variant_rcp(const ForceArgs& a, int64_t n, int rcp, unsigned grid, PairConsts c,
+                                      cudaStream_t s) {
+#define LJ_V(R)                                                                                                 \
+    k_force_variant<G, LAYOUT, R><<<grid, kForceThreads, 0, s>>>(a.q, a.p, n, a.row_begin, a.rows, a.npart, a.ptr, \
+                                                                 a.list, c, a.n_inter)
+    switch (rcp) {
+        case LJ_RCP_NEWTON3: LJ_V(LJ_RCP_NEWTON3); break;
+        case LJ_RCP_NEWTON2: LJ_V(LJ_RCP_NEWTON2); break;
+        case LJ_RCP_APPROX: LJ_V(LJ_RCP_APPROX); break;
+        case LJ_RCP_IEEE: LJ_V(LJ_RCP_IEEE); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef LJ_V
+    return cudaGetLastError();
+}
+
+template <int G>
+static cudaError_t launch_variant_g(const ForceArgs& a, int64_t n, int layout, int rcp, unsigned grid, PairConsts c,
+                                    cudaStream_t s) {
+    switch (layout) {
+        case LJ_LAYOUT_AOS4: return launch_variant_rcp<G, LJ_LAYOUT_AOS4>(a, n, rcp, grid, c, s);
+        case LJ_LAYOUT_SOA: return launch_variant_rcp<G, LJ_LAYOUT_SOA>(a, n, rcp, grid, c, s);
+        case LJ_LAYOUT_AOS3: return launch_variant_rcp<G, LJ_LAYOUT_AOS3>(a, n, rcp, grid, c, s);
+        case LJ_LAYOUT_AOS8: return launch_variant_rcp<G, LJ_LAYOUT_AOS8>(a, n, rcp, grid, c, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_force_variant(const ForceArgs& a, int64_t n, int layout, int rcp, int lanes, cudaStream_t s) {
+    if (a.rows <= 0) return cudaSuccess;
+    PairConsts c = make_consts(a);
+    const unsigned grid = (unsigned)((a.rows * (int64_t)lanes + kForceThreads - 1) / kForceThreads);
+    cudaError_t e = lanes == 4 ? launch_variant_g<4>(a, n, layout, rcp, grid, c, s)
+                  : lanes == 8 ? launch_variant_g<8>(a, n, layout, rcp, grid, c, s)
+                               : cudaErrorInvalidValue;
+    g_launches++;
+    return e;
 }
 
 cudaError_t launch_force_ordered(const ForceArgs& a, cudaStream_t s) {

@@ -18,12 +18,15 @@ LIB_PATH = os.path.join(_HERE, "liblj.so")
 
 LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 192   # include/liblj.h
+LAYOUTS = {"aos4": 0, "soa": 1, "aos3": 2, "aos8": 3}                    # LJ_LAYOUT_*
+RECIPROCALS = {"newton3": 0, "newton2": 1, "approx": 2, "ieee": 3}       # LJ_RCP_*
 
 # every symbol include/liblj.h declares
 EXPORTS = (
     "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_rebuild",
     "lj_cell_order",
-    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_gather_probe", "lj_list_interior", "lj_integrate",
+    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_force_step_variant", "lj_gather_probe",
+    "lj_list_interior", "lj_integrate",
     "lj_wrap",
     "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
     "lj_version",
@@ -70,6 +73,7 @@ def load() -> ctypes.CDLL:
         "lj_permute_rows": (st, [vp, vp, vp, i64, vp]),
         "lj_force_step": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, vp]),
         "lj_force_step_ex": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, i32, i32, vp, vp]),
+        "lj_force_step_variant": (st, [i32, i32, vp, vp, i64, Geom, d, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_gather_probe": (st, [vp, i64, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_list_interior": (st, [i64, i64, vp, vp, vp, vp, vp]),
         "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
@@ -279,6 +283,21 @@ def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRLis
         lanes_per_row = 8 | (2 << 8)   # padded rows: 8 lanes per row measured faster (0.82 vs 0.87 ms, config 4)
     _check(load().lj_force_step_ex(_ptr(q), _ptr(p), q.shape[0], g, float(dt), int(lst.half), *_list_args(lst),
                                    int(lanes_per_row), int(ordered), _ptr(n_interactions), _stream()))
+
+
+def force_step_variant(layout: str, rcp: str, q: torch.Tensor, p: torch.Tensor | None, n: int, g: Geom,
+                       dt: float, lst: CSRList, lanes_per_row: int = 4,
+                       n_interactions: torch.Tensor | None = None) -> None:
+    """Paper-variant ablation (lj_force_step_variant): q/p are flat float64 CUDA
+    tensors in `layout` ("aos4", "soa", "aos3", "aos8"; p unused for aos8), 1/r^2
+    by `rcp` ("newton3", "newton2", "approx", "ieee")."""
+    for t in (q, p):
+        if t is not None and not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise TypeError("force_step_variant: q/p must be contiguous CUDA float64 tensors")
+    if lst.half:
+        raise ValueError("force_step_variant: full lists only")
+    _check(load().lj_force_step_variant(LAYOUTS[layout], RECIPROCALS[rcp], _ptr(q), _ptr(p), int(n), g, float(dt),
+                                        *_list_args(lst), int(lanes_per_row), _ptr(n_interactions), _stream()))
 
 
 def gather_probe(q: torch.Tensor, lst: CSRList, lanes_per_row: int = 0, sink: torch.Tensor | None = None) -> None:

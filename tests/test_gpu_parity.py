@@ -487,3 +487,51 @@ def test_list_interior_and_row_views(lj, dev, systems, rows):
         if y > x:
             lj.force_step(q, pb, g, w.dt, gl.rows_view(x, y))
     assert torch.equal(pa, pb)
+
+
+@pytest.mark.parametrize("layout", ["aos4", "soa", "aos3", "aos8"])
+@pytest.mark.parametrize("lanes", [4, 8])
+def test_layout_variants_bit_identical(lj, dev, systems, layout, lanes):
+    """NEXT-4 ablation: the paper's layouts change only the gathers and the
+    momentum commit -- momenta bit-identical to the AoS4 (library) layout, and
+    within C-12 of the oracle."""
+    import sys
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1] / "tools"))
+    from ablation import from_layout, to_layout
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    p0 = np.random.default_rng(61).normal(0, 1, (w.n, 3))
+    p = to_dev(p0, dev)
+    gl = lj.build_list(q, g, False)
+    ql = to_layout(q, layout, p)
+    pl = None if layout == "aos8" else to_layout(p, layout)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    lj.force_step_variant(layout, "newton3", ql, pl, w.n, g, w.dt, gl, lanes, n_interactions=cnt)
+    got = from_layout(ql if layout == "aos8" else pl, layout, w.n).cpu().numpy()
+    pa = to_dev(p0, dev)
+    lj.force_step(q, pa, g, w.dt, gl, lanes_per_row=lanes | (2 << 8))
+    assert np.array_equal(got, from_dev(pa))
+    ref, S, _ = oracle_force(w, p0, False)
+    assert oracle.parity_error(got, ref, S) <= TOL
+    assert int(cnt.item()) == _entries_inside(w, False)
+
+
+@pytest.mark.parametrize("rcp,ok", [("newton3", True), ("ieee", True), ("approx", False)])
+def test_reciprocal_variants(lj, dev, systems, rcp, ok):
+    """NEXT-4: 1/r^2 by MUFU.RCP64H alone misses the 1e-12 bar (why the library
+    adds a Newton step); the cubic step and the IEEE reciprocal meet it."""
+    import sys
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1] / "tools"))
+    from ablation import from_layout, to_layout
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    p0 = np.random.default_rng(62).normal(0, 1, (w.n, 3))
+    p = to_dev(p0, dev)
+    gl = lj.build_list(q, g, False)
+    pl = to_layout(p, "aos4")
+    lj.force_step_variant("aos4", rcp, to_layout(q, "aos4"), pl, w.n, g, w.dt, gl, 4)
+    ref, S, _ = oracle_force(w, p0, False)
+    e = oracle.parity_error(from_layout(pl, "aos4", w.n).cpu().numpy(), ref, S)
+    assert (e <= TOL) == ok, e
