@@ -202,7 +202,10 @@ def main():
     dev = torch.device("cuda", local)
     comm = None
     if world > 1 or "MASTER_ADDR" in os.environ:   # torchrun (any N): NCCL process group
-        dist.init_process_group("nccl", device_id=dev)
+        # failure detection: NCCL errors/timeouts abort the collective instead of hanging the job
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+        import datetime
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=600))
         comm = dist.group.WORLD
 
     def barrier():
