@@ -50,6 +50,8 @@ def parse():
                     help="storage order; default: config 2 shuffled, 3 cell, 4/5 cell (re-sorted at every rebuild)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="P > 1: blocking all-gather (no comm/compute overlap)")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
+                    help="P > 1: position exchange between rebuilds (halo = only the rows each rank's list reads)")
     ap.add_argument("--energy-every", type=int, default=None,
                     help="NVE energy sample interval in timed steps (default: config 5 -> steps/20, else off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -224,7 +226,7 @@ def main():
     rb, re_ = md.row_range(w.n, rank, world)
     be = md.LibBackend(w.n, g, rb, re_, dev, half=half)
     sim = md.LeapfrogMD(be, w.q, w.p, g, w.dt, rank, world, comm, reorder=(order == "cell"),
-                        overlap=not args.no_overlap)
+                        overlap=not args.no_overlap, exchange=args.exchange)
     if not force_only:
         sim.start_leapfrog()   # p_0 -> p_{-1/2}
 
@@ -396,8 +398,9 @@ def main():
             "config": {"workload": f"config{args.config}", "n_atoms": w.n, "list": "half" if half else "full",
                        "order": order + (" (re-sorted at every rebuild)" if order == "cell" and not force_only else ""),
                        "dt": w.dt, "rc": w.rc, "rs": w.rs, "parallelism": f"rows/{world}",
-                       "exchange": ("async all-gather overlapped with the interior rows' force" if sim.overlap
-                                    else ("all-gather" if world > 1 else "none (1 rank)")),
+                       "exchange": (("halo" if sim.halo else "all-gather")
+                                    + (" (async, overlapped with the interior rows' force)" if sim.overlap else "")
+                                    if (world > 1 or sim.collective) else "none (1 rank)"),
                        "l2": "inputs larger than L2 (CSR list %.2f GB + records)" % (4 * sim.lst.n_entries / 1e9),
                        "rebuilds_in_timed_steps": rebuilds},
             "ms_per_force_step": force_avg,

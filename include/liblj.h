@@ -199,6 +199,17 @@ lj_status lj_gather_probe(const double *q, int64_t n, int64_t row_begin, int64_t
 lj_status lj_list_interior(int64_t row_begin, int64_t row_end, const int32_t *number_of_partners,
                            const int64_t *pointer, const int32_t *sorted_list, int64_t *out, void *stream);
 
+/* Halo requests of a row-split list (halo exchange in place
+ * of the all-gather): the P owner slabs are rows [bounds[s], bounds[s+1])
+ * (bounds: device, P + 1 int64, ascending, bounds[P] = n); out (device, 2P
+ * int64) = for every s, {min, max} of the partner indices of rows [row_begin,
+ * row_end) that lie in slab s, or {INT64_MAX, -1} if none.  The force on these
+ * rows reads exactly positions [min, max] of each slab it touches.  1 <= P <=
+ * 64.  Asynchronous. */
+lj_status lj_list_partner_ranges(int64_t row_begin, int64_t row_end, const int32_t *number_of_partners,
+                                 const int64_t *pointer, const int32_t *sorted_list, const int64_t *bounds, int P,
+                                 int64_t *out, void *stream);
+
 /* ---- integration and bookkeeping (§8(a) a7, a9) --------------------------- */
 
 /* Drift q_i += p_i dt for atoms [begin, end) (mass 1), bit-identical to the

@@ -385,6 +385,19 @@ lj_status lj_list_interior(int64_t row_begin, int64_t row_end, const int32_t* nu
     return LJ_OK;
 }
 
+lj_status lj_list_partner_ranges(int64_t row_begin, int64_t row_end, const int32_t* number_of_partners,
+                                 const int64_t* pointer, const int32_t* sorted_list, const int64_t* bounds, int P,
+                                 int64_t* out, void* stream) {
+    if (row_begin < 0 || row_end < row_begin) return fail(LJ_ERR_ARG, "partner_ranges: bad row range");
+    if (P < 1 || P > 64) return fail(LJ_ERR_ARG, "partner_ranges: need 1 <= P <= 64 (got %d)", P);
+    if (!out || !bounds || (row_end > row_begin && (!number_of_partners || !pointer || !sorted_list)))
+        return fail(LJ_ERR_ARG, "partner_ranges: null pointer");
+    LJ_CUDA(launch_partner_ranges(row_begin, row_end, number_of_partners, pointer, sorted_list, bounds, P, out,
+                                  (cudaStream_t)stream),
+            "lj_list_partner_ranges");
+    return LJ_OK;
+}
+
 lj_status lj_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, void* stream) {
     if (begin < 0 || end < begin || end > (int64_t)INT32_MAX)
         return fail(LJ_ERR_ARG, "integrate: bad range [%lld,%lld)", (long long)begin, (long long)end);

@@ -92,6 +92,8 @@ cudaError_t launch_integrate(double* q, const double* p, int64_t begin, int64_t 
 cudaError_t launch_wrap(double* q, double* q_ref, int64_t n, double L, cudaStream_t s);
 cudaError_t launch_max_disp(const double* q, const double* q_ref, int64_t begin, int64_t end, double* out,
                             cudaStream_t s);
+cudaError_t launch_partner_ranges(int64_t row_begin, int64_t row_end, const int32_t* npart, const int64_t* ptr,
+                                  const int32_t* list, const int64_t* bounds, int P, int64_t* out, cudaStream_t s);
 cudaError_t launch_list_interior(int64_t row_begin, int64_t row_end, const int32_t* npart, const int64_t* ptr,
                                  const int32_t* list, int64_t* out, cudaStream_t s);
 cudaError_t launch_energy(const double* q, const double* p, int64_t row_begin, int64_t rows, const int32_t* npart,

@@ -2,6 +2,8 @@
 // AoS4 pack/unpack, drift, wrap + bookkeeping snapshot, max displacement, energy.
 // All are HBM-streaming (one pass over 32-B records); integrate, wrap and the
 // displacement are bit-identical to the oracle (explicit _rn intrinsics).
+#include <climits>
+
 #include "lj_internal.cuh"
 
 namespace lj {
@@ -169,6 +171,69 @@ __global__ void k_list_interior(int64_t row_begin, int64_t row_end, const int32_
     }
 }
 
+// Halo requests: for every owner slab s (rows
+// [bounds[s], bounds[s+1])), the smallest and largest partner index of the own
+// rows that falls in it.  Partners of a row ascend, so each owner's entries in a
+// row are one contiguous run: a warp scans its row, lanes reduce per owner in
+// shared memory, one global atomic per block and owner.
+constexpr int kMaxRanks = 64;
+
+__global__ void k_partner_ranges(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ npart,
+                                 const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
+                                 const int64_t* __restrict__ bounds, int P, long long* out) {
+    __shared__ long long s_lo[kMaxRanks], s_hi[kMaxRanks];
+    __shared__ long long s_b[kMaxRanks + 1];
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+        s_lo[k] = LLONG_MAX;
+        s_hi[k] = -1;
+    }
+    for (int k = threadIdx.x; k <= P; k += blockDim.x) s_b[k] = bounds[k];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < row_end - row_begin;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int n = npart[r];
+        const int32_t* l = list + ptr[r];
+        int prev_owner = -1;   // owner of the entry before this chunk (warp-uniform)
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            const long long j = k < n ? l[k] : -1;
+            int own = -1;
+            if (k < n) {
+                int lo = 0, hi = P;   // owner: largest s with s_b[s] <= j
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_b[mid] <= j) lo = mid; else hi = mid;
+                }
+                own = lo;
+            }
+            // ascending entries: one owner's entries are a contiguous run -- only run
+            // starts and ends touch the shared minima and maxima
+            int before = __shfl_up_sync(0xffffffffu, own, 1);
+            if (lane == 0) before = prev_owner;
+            int after = __shfl_down_sync(0xffffffffu, own, 1);
+            if (lane == 31 || k + 1 >= n) after = -2;
+            if (own >= 0 && own != before) atomicMin(&s_lo[own], j);
+            if (own >= 0 && own != after) atomicMax(&s_hi[own], j);
+            prev_owner = __shfl_sync(0xffffffffu, own, 31);
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+        if (s_hi[k] >= 0) {
+            atomicMin(&out[2 * k], s_lo[k]);
+            atomicMax(&out[2 * k + 1], s_hi[k]);
+        }
+    }
+}
+
+__global__ void k_init_ranges(long long* out, int P) {
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+        out[2 * k] = LLONG_MAX;
+        out[2 * k + 1] = -1;
+    }
+}
+
 __global__ void k_init_interior(unsigned long long* out, int64_t row_begin, int64_t row_end) {
     out[0] = (unsigned long long)row_begin;
     out[1] = (unsigned long long)row_end;
@@ -183,6 +248,19 @@ cudaError_t launch_list_interior(int64_t row_begin, int64_t row_end, const int32
     if (row_end > row_begin) {
         k_list_interior<<<grid_for((row_end - row_begin) * 32, kThreads, 148 * 16), kThreads, 0, s>>>(
             row_begin, row_end, npart, ptr, list, (unsigned long long*)out);
+        g_launches++;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_partner_ranges(int64_t row_begin, int64_t row_end, const int32_t* npart, const int64_t* ptr,
+                                  const int32_t* list, const int64_t* bounds, int P, int64_t* out, cudaStream_t s) {
+    if (P < 1 || P > kMaxRanks) return cudaErrorInvalidValue;
+    k_init_ranges<<<1, 64, 0, s>>>((long long*)out, P);
+    g_launches++;
+    if (row_end > row_begin) {
+        k_partner_ranges<<<grid_for((row_end - row_begin) * 32, kThreads, 148 * 8), kThreads, 0, s>>>(
+            row_begin, row_end, npart, ptr, list, bounds, P, (long long*)out);
         g_launches++;
     }
     return cudaGetLastError();

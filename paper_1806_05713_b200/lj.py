@@ -76,6 +76,7 @@ def load() -> ctypes.CDLL:
         "lj_force_step_variant": (st, [i32, i32, vp, vp, i64, Geom, d, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_gather_probe": (st, [vp, i64, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_list_interior": (st, [i64, i64, vp, vp, vp, vp, vp]),
+        "lj_list_partner_ranges": (st, [i64, i64, vp, vp, vp, vp, i32, vp, vp]),
         "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
         "lj_wrap": (st, [vp, vp, i64, d, vp]),
         "lj_max_displacement": (st, [vp, vp, i64, i64, vp, vp]),
@@ -320,6 +321,19 @@ def list_interior(lst: CSRList) -> tuple[int, int]:
                                    _ptr(lst.sorted_list), _ptr(out), _stream()))
     a, b = out.tolist()
     return int(a), int(b)
+
+
+def list_partner_ranges(lst: CSRList, bounds: list[int]) -> list[tuple[int, int]]:
+    """For every owner slab s = rows [bounds[s], bounds[s+1]): (min, max) partner index of the
+    list's rows inside it, or None (lj_list_partner_ranges; one readback)."""
+    P = len(bounds) - 1
+    dev = lst.pointer.device
+    b = torch.tensor(bounds, dtype=torch.int64, device=dev)
+    out = torch.empty(2 * P, dtype=torch.int64, device=dev)
+    _check(load().lj_list_partner_ranges(lst.row_begin, lst.row_end, _ptr(lst.number_of_partners), _ptr(lst.pointer),
+                                         _ptr(lst.sorted_list), _ptr(b), P, _ptr(out), _stream()))
+    v = out.tolist()
+    return [None if v[2 * s + 1] < 0 else (int(v[2 * s]), int(v[2 * s + 1])) for s in range(P)]
 
 
 def integrate(q: torch.Tensor, p: torch.Tensor, dt: float, begin: int = 0, end: int | None = None) -> None:

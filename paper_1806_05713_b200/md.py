@@ -85,6 +85,10 @@ class LibBackend:
         """Rows [A, B) whose partners are all own rows (lj_list_interior)."""
         return lj.list_interior(lst)
 
+    def partner_ranges(self, lst, bounds):
+        """Per owner slab, (min, max) partner index of lst's rows (lj_list_partner_ranges)."""
+        return lj.list_partner_ranges(lst, bounds)
+
     def integrate(self, q, p, dt, b, e):
         lj.integrate(q, p, dt, b, e)
 
@@ -109,7 +113,8 @@ class LeapfrogMD:
     torch.distributed process group (NCCL on GPUs, gloo in CPU tests)."""
 
     def __init__(self, backend, q_xyz, p_xyz, g: lj.Geom, dt: float, rank: int = 0, world: int = 1, comm=None,
-                 count_interactions: bool = True, reorder: bool = True, overlap: bool | None = None):
+                 count_interactions: bool = True, reorder: bool = True, overlap: bool | None = None,
+                 exchange: str = "allgather"):
         self.be, self.g, self.dt = backend, g, float(dt)
         self.n = q_xyz.shape[0]
         self.rank, self.world, self.comm = rank, world, comm
@@ -138,6 +143,14 @@ class LeapfrogMD:
         self.overlap = can if overlap is None else (bool(overlap) and can)
         self._pending = None                  # async all-gather of q in flight
         self.interior_rows = (self.rb, self.re)
+        # halo exchange: between rebuilds each rank receives only the
+        # position rows its list reads from other ranks (lj_list_partner_ranges) instead of
+        # all of them; rebuilds, kdk_step and gather_all_positions() use the full all-gather
+        if exchange not in ("allgather", "halo"):
+            raise ValueError("exchange must be 'allgather' or 'halo'")
+        self.halo = exchange == "halo" and self.collective and world > 1 and hasattr(backend, "partner_ranges")
+        self._halo_plan = None                # (sends [(rank, lo, hi)], recvs [(rank, lo, hi)])
+        self._stale = False                   # other ranks' rows outside the halo are out of date
         self._rebuild()
 
     # ---- collectives (no-ops for one rank) ----
@@ -163,19 +176,64 @@ class LeapfrogMD:
     def _allgather_q(self):
         self.sync_positions()
         self._allgather(self.q)
+        self._stale = False
 
     def _allgather_q_async(self):
         """Start the in-place all-gather of the own position rows (completed by sync_positions)."""
         if self.collective:
             own = self.q[self.rb:self.re]
-            self._pending = dist.all_gather_into_tensor(self.q, own.clone() if self._gloo() else own,
-                                                        group=self.comm, async_op=True)
+            self._pending = [dist.all_gather_into_tensor(self.q, own.clone() if self._gloo() else own,
+                                                         group=self.comm, async_op=True)]
 
     def sync_positions(self):
-        """Complete a pending all-gather: afterwards every rank's q holds all positions."""
+        """Complete a pending exchange: afterwards q holds every position the own rows' forces read
+        (all positions after an all-gather; see gather_all_positions for the halo mode)."""
         if self._pending is not None:
-            self._pending.wait()
+            for w in self._pending:
+                w.wait()
             self._pending = None
+
+    def gather_all_positions(self):
+        """Make every rank's q hold all current positions (a full all-gather in the halo mode)."""
+        self.sync_positions()
+        if self._stale:
+            self._allgather_q()
+
+    # ---- halo exchange (NEXT-2) ----
+    def _plan_halo(self):
+        """After a build: which own rows every other rank reads, and which rows of theirs we read."""
+        bounds = [row_range(self.n, s, self.world)[0] for s in range(self.world)] + [self.n]
+        need = self.be.partner_ranges(self.lst, bounds)
+        mine = torch.zeros((self.world, 2), dtype=torch.int64, device=self.q.device)
+        for s, r in enumerate(need):
+            if s != self.rank and r is not None:
+                mine[s, 0], mine[s, 1] = r[0], r[1] + 1
+        table = torch.empty((self.world * self.world, 2), dtype=torch.int64, device=self.q.device)
+        dist.all_gather_into_tensor(table, mine, group=self.comm)
+        table = table.view(self.world, self.world, 2).tolist()   # table[a][s] = rows of s that a reads
+        sends = [(a, *table[a][self.rank]) for a in range(self.world)
+                 if a != self.rank and table[a][self.rank][1] > table[a][self.rank][0]]
+        recvs = [(s, *table[self.rank][s]) for s in range(self.world)
+                 if s != self.rank and table[self.rank][s][1] > table[self.rank][s][0]]
+        self._halo_plan = (sends, recvs)
+
+    def _halo_exchange(self, async_op: bool):
+        sends, recvs = self._halo_plan
+        ops = [dist.P2POp(dist.isend, self.q[lo:hi], a, group=self.comm) for a, lo, hi in sends]
+        ops += [dist.P2POp(dist.irecv, self.q[lo:hi], s, group=self.comm) for s, lo, hi in recvs]
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        self._stale = True
+        if async_op:
+            self._pending = list(reqs)
+        else:
+            for r in reqs:
+                r.wait()
+
+    def halo_bytes(self) -> int:
+        """Position bytes this rank receives per step in the halo mode."""
+        if self._halo_plan is None:
+            return 0
+        return sum(hi - lo for _, lo, hi in self._halo_plan[1]) * 32
 
     def _gloo(self):
         return dist.get_backend(self.comm) == "gloo"
@@ -201,10 +259,12 @@ class LeapfrogMD:
     def _rebuild(self):
         """Wrap, (optionally) re-sort the atoms into cell order (§8(a) a3), snapshot
         q_ref and rebuild the own-row list (§8(a) a2-a4)."""
-        self.sync_positions()
+        self.gather_all_positions()
         self._rebuild_lists()
         if self.overlap:
             self.interior_rows = self.be.interior(self.lst)
+        if self.halo:
+            self._plan_halo()
 
     def _rebuild_lists(self):
         if self.reorder:
@@ -264,6 +324,8 @@ class LeapfrogMD:
             self._allgather_q()
             self._rebuild()
             self.stats.rebuilds += 1
+        elif self.halo:
+            self._halo_exchange(async_op=self.overlap)
         elif self.overlap:
             self._allgather_q_async()
         else:

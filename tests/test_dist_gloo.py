@@ -71,6 +71,15 @@ class OracleBackend:
                     b = min(b, i)
         return a, b
 
+    def partner_ranges(self, lst, bounds):
+        """Same definition as lj_list_partner_ranges, in numpy."""
+        j = lst.sorted_list[:lst.n_entries].astype(np.int64)
+        out = []
+        for s in range(len(bounds) - 1):
+            m = j[(j >= bounds[s]) & (j < bounds[s + 1])]
+            out.append((int(m.min()), int(m.max())) if len(m) else None)
+        return out
+
     def integrate(self, q, p, dt, b, e):
         q[:, :3] = torch.as_tensor(oracle.integrate(self._xyz(q), self._xyz(p), dt, b, e))
 
@@ -95,17 +104,21 @@ def make_system(n_drop, cells=8):
     return w, q, p
 
 
-def run(rank, world, n_drop, reorder, steps, comm=None, overlap=None):
+def run(rank, world, n_drop, reorder, steps, comm=None, overlap=None, exchange="allgather"):
     # overlap needs slabs wider than 2 r_s to have interior rows: 12^3 FCC cells (L = 19)
-    w, q, p = make_system(n_drop, 12 if overlap else 8)
+    w, q, p = make_system(n_drop, 12 if (overlap or exchange == "halo") else 8)
     g = lj.geom(w.L, w.rc, w.rs)
     rb, re_ = md.row_range(q.shape[0], rank, world)
     sim = md.LeapfrogMD(OracleBackend(q.shape[0], g, rb, re_), q, p, g, w.dt, rank, world, comm,
-                        count_interactions=False, reorder=reorder, overlap=overlap)
+                        count_interactions=False, reorder=reorder, overlap=overlap, exchange=exchange)
+    if world > 2 and exchange == "halo":
+        assert sim.halo and 0 < sim.halo_bytes() < (q.shape[0] - (re_ - rb)) * 32, "a halo, not everything"
     if world > 1 and overlap:
         assert sim.overlap
         a, b = sim.interior_rows
-        assert rb < a < b < re_, "the slabs must have interior and boundary rows"
+        assert rb <= a <= b <= re_
+        if world == 2:
+            assert rb < a < b < re_, "the slabs must have interior and boundary rows"
     sim.half_kick()
     for _ in range(steps):
         sim.step()
@@ -117,12 +130,12 @@ def run(rank, world, n_drop, reorder, steps, comm=None, overlap=None):
     return sim.q.numpy().copy(), p_full.numpy().copy(), sim.stats.rebuilds, e
 
 
-def _worker(rank, world, port, n_drop, reorder, steps, outdir, overlap=None):
+def _worker(rank, world, port, n_drop, reorder, steps, outdir, overlap=None, exchange="allgather"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        q, p, rb, e = run(rank, world, n_drop, reorder, steps, dist.group.WORLD, overlap)
+        q, p, rb, e = run(rank, world, n_drop, reorder, steps, dist.group.WORLD, overlap, exchange)
         np.savez(os.path.join(outdir, f"r{rank}.npz"), q=q, p=p, rb=rb, e=np.array(e))
     finally:
         dist.destroy_process_group()
@@ -136,17 +149,20 @@ def free_port():
     return port
 
 
-@pytest.mark.parametrize("n_drop,reorder,overlap", [(0, True, False), (0, False, False), (3, True, None),
-                                                    (0, True, True), (0, False, True)])
-def test_two_ranks_equal_one_rank(tmp_path, n_drop, reorder, overlap):
-    """overlap=True: the all-gather runs asynchronously while the interior rows'
-    forces are computed -- still bit-identical."""
+@pytest.mark.parametrize("world,n_drop,reorder,overlap,exchange", [
+    (2, 0, True, False, "allgather"), (2, 0, False, False, "allgather"), (2, 3, True, None, "allgather"),
+    (2, 0, True, True, "allgather"), (2, 0, False, True, "allgather"),
+    (2, 0, True, False, "halo"), (3, 0, True, True, "halo"), (3, 0, False, False, "halo")])
+def test_ranks_equal_one_rank(tmp_path, world, n_drop, reorder, overlap, exchange):
+    """overlap=True: the position exchange runs asynchronously while the interior
+    rows' forces are computed; exchange="halo": only the rows
+    each rank's list reads are sent between rebuilds (NEXT-2) -- still bit-identical."""
     steps = 12        # T = 1, dt = 0.01: the list is rebuilt every ~4-5 steps
-    q1, p1, rb1, e1 = run(0, 1, n_drop, reorder, steps, overlap=overlap)
+    q1, p1, rb1, e1 = run(0, 1, n_drop, reorder, steps, overlap=overlap, exchange=exchange)
     assert rb1 >= 2, "the test must exercise rebuilds"
-    mp.start_processes(_worker, args=(2, free_port(), n_drop, reorder, steps, str(tmp_path), overlap), nprocs=2,
-                       start_method="spawn")
-    for r in range(2):
+    mp.start_processes(_worker, args=(world, free_port(), n_drop, reorder, steps, str(tmp_path), overlap, exchange),
+                       nprocs=world, start_method="spawn")
+    for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
         assert np.array_equal(d["q"], q1)
         assert np.array_equal(d["p"], p1)

@@ -535,3 +535,18 @@ def test_reciprocal_variants(lj, dev, systems, rcp, ok):
     ref, S, _ = oracle_force(w, p0, False)
     e = oracle.parity_error(from_layout(pl, "aos4", w.n).cpu().numpy(), ref, S)
     assert (e <= TOL) == ok, e
+
+
+@pytest.mark.parametrize("P,r", [(1, 0), (4, 1), (8, 0), (8, 7), (3, 2)])
+def test_list_partner_ranges(lj, dev, systems, P, r):
+    """lj_list_partner_ranges against its definition (numpy over the oracle's list)."""
+    w = systems[3]
+    g = lj.geom(w.L, w.rc, w.rs)
+    bounds = [w.n * s // P for s in range(P)] + [w.n]
+    rb, re_ = bounds[r], bounds[r + 1]
+    gl = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=True).build(to_dev(w.q, dev))
+    got = lj.list_partner_ranges(gl, bounds)
+    j = oracle.list_cells(w.q, w.L, w.rs, False, rb, re_).sorted_list.astype(np.int64)
+    for s in range(P):
+        m = j[(j >= bounds[s]) & (j < bounds[s + 1])]
+        assert got[s] == ((int(m.min()), int(m.max())) if len(m) else None)
