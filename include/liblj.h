@@ -93,7 +93,12 @@ lj_status lj_build_list(const double *q, int64_t n, lj_geom g, int half,
  * compact CSR; every consumer of a list (force, energy) reads only
  * [pointer[r], pointer[r] + number_of_partners[r]). */
 #define LJ_LIST_PADDED 1
-#define LJ_PADDED_ROW_STRIDE 192
+#ifndef LJ_PADDED_ROW_STRIDE
+/* 196 entries = 784 B: not a multiple of the 128-B line, so the rows a warp
+ * reads do not all start on the same DRAM channel / L2 slice (strides of 640 or
+ * 768 B made the force step 10 % slower, tools/stride_sweep.sh). */
+#define LJ_PADDED_ROW_STRIDE 196
+#endif
 
 /* lj_build_list with layout flags (0 = compact CSR, as lj_build_list).  With
  * LJ_LIST_PADDED, capacity must be >= rows * LJ_PADDED_ROW_STRIDE (else

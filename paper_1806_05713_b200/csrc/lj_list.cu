@@ -30,7 +30,7 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 }  // namespace
-constexpr int kRowCap = 192;     // v2: scratch entries per row (longer rows -> direct second pass)
+constexpr int kRowCap = LJ_PADDED_ROW_STRIDE;   // scratch / padded entries per row (longer rows -> direct pass)
 namespace {
 constexpr int kRowBuf = 512;     // fallback: per-warp row buffer (entries)
 constexpr int kCellBuf = 256;    // per-warp cell buffer for the in-cell sort

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblj.so")
 
 LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
-LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 192   # include/liblj.h
+LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 196   # include/liblj.h
 LAYOUTS = {"aos4": 0, "soa": 1, "aos3": 2, "aos8": 3}                    # LJ_LAYOUT_*
 RECIPROCALS = {"newton3": 0, "newton2": 1, "approx": 2, "ieee": 3}       # LJ_RCP_*
 
@@ -280,8 +280,6 @@ def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRLis
     _rec(p, "p")
     if n_interactions is not None and not (n_interactions.is_cuda and n_interactions.dtype == torch.int64):
         raise TypeError("n_interactions must be a CUDA int64 tensor")
-    if lanes_per_row == 0 and lst.padded and not lst.half and not ordered:
-        lanes_per_row = 8 | (2 << 8)   # padded rows: 8 lanes per row measured faster (0.82 vs 0.87 ms, config 4)
     _check(load().lj_force_step_ex(_ptr(q), _ptr(p), q.shape[0], g, float(dt), int(lst.half), *_list_args(lst),
                                    int(lanes_per_row), int(ordered), _ptr(n_interactions), _stream()))
 
@@ -306,8 +304,6 @@ def gather_probe(q: torch.Tensor, lst: CSRList, lanes_per_row: int = 0, sink: to
     _rec(q, "q")
     if sink is None:
         sink = torch.zeros(1, dtype=torch.float64, device=q.device)
-    if lanes_per_row == 0 and lst.padded:
-        lanes_per_row = 8   # the lanes force_step uses on padded lists
     _check(load().lj_gather_probe(_ptr(q), q.shape[0], lst.row_begin, lst.row_end, _ptr(lst.number_of_partners),
                                   _ptr(lst.pointer), _ptr(lst.sorted_list), int(lanes_per_row), _ptr(sink),
                                   _stream()))
