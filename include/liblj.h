@@ -221,6 +221,11 @@ lj_status lj_list_partner_ranges(int64_t row_begin, int64_t row_end, const int32
  * oracle (no FMA).  Positions are not wrapped. */
 lj_status lj_integrate(double *q, const double *p, int64_t begin, int64_t end, double dt, void *stream);
 
+/* lj_integrate followed by lj_max_displacement(q, q_ref, begin, end, max_disp)
+ * in one pass over the own rows (both results bit-identical to the two calls). */
+lj_status lj_integrate_displacement(double *q, const double *p, const double *q_ref, int64_t begin, int64_t end,
+                                   double dt, double *max_disp, void *stream);
+
 /* Wrap q into [0,L) (x -= L floor(x/L); x -= L if x >= L) for atoms [0,n) and,
  * if q_ref != NULL, copy the wrapped records to q_ref (the bookkeeping
  * reference of PAPER.md:190-192). */

@@ -408,6 +408,19 @@ lj_status lj_integrate(double* q, const double* p, int64_t begin, int64_t end, d
     return LJ_OK;
 }
 
+lj_status lj_integrate_displacement(double* q, const double* p, const double* q_ref, int64_t begin, int64_t end,
+                                   double dt, double* max_disp, void* stream) {
+    if (begin < 0 || end < begin || end > (int64_t)INT32_MAX)
+        return fail(LJ_ERR_ARG, "integrate_displacement: bad range [%lld,%lld)", (long long)begin, (long long)end);
+    if (!max_disp || (end > begin && (!q || !p || !q_ref))) return fail(LJ_ERR_ARG, "integrate_displacement: null pointer");
+    if (!aligned32(q) || !aligned32(p) || !aligned32(q_ref))
+        return fail(LJ_ERR_ARG, "integrate_displacement: not 32-byte aligned");
+    if (!std::isfinite(dt)) return fail(LJ_ERR_ARG, "integrate_displacement: dt not finite");
+    LJ_CUDA(launch_integrate_disp(q, p, q_ref, begin, end, dt, max_disp, (cudaStream_t)stream),
+            "lj_integrate_displacement");
+    return LJ_OK;
+}
+
 lj_status lj_wrap(double* q, double* q_ref, int64_t n, double L, void* stream) {
     LJ_TRY(check_n(n));
     if (!(L > 0.0) || !std::isfinite(L)) return fail(LJ_ERR_ARG, "wrap: L must be > 0");

@@ -89,6 +89,8 @@ cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cud
 cudaError_t launch_pack(const double* xyz, double* out, int64_t n, cudaStream_t s);
 cudaError_t launch_unpack(const double* in, double* xyz, int64_t n, cudaStream_t s);
 cudaError_t launch_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, cudaStream_t s);
+cudaError_t launch_integrate_disp(double* q, const double* p, const double* q_ref, int64_t begin, int64_t end,
+                                  double dt, double* out, cudaStream_t s);
 cudaError_t launch_wrap(double* q, double* q_ref, int64_t n, double L, cudaStream_t s);
 cudaError_t launch_max_disp(const double* q, const double* q_ref, int64_t begin, int64_t end, double* out,
                             cudaStream_t s);

@@ -46,6 +46,11 @@ __global__ void k_integrate(rec4* __restrict__ q, const rec4* __restrict__ p, in
     }
 }
 
+// Drift fused with the bookkeeping displacement (one pass over the own rows):
+// q_i += p_i dt exactly as k_integrate, then |q_i - q_ref_i| exactly as k_max_disp.
+__global__ void k_integrate_disp(rec4* __restrict__ q, const rec4* __restrict__ p, const rec4* __restrict__ q_ref,
+                                 int64_t begin, int64_t end, double dt, unsigned long long* out);
+
 __device__ __forceinline__ double wrap1(double x, double L) {
     double w = __dsub_rn(x, __dmul_rn(L, floor(__ddiv_rn(x, L))));
     if (w >= L) w = __dsub_rn(w, L);
@@ -101,6 +106,25 @@ __global__ void k_max_disp(const rec4* __restrict__ q, const rec4* __restrict__ 
         double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y), dz = __dsub_rn(a.z, b.z);
         double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
         m = fmax(m, d);
+    }
+    m = block_max(m);
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_integrate_disp(rec4* __restrict__ q, const rec4* __restrict__ p, const rec4* __restrict__ q_ref,
+                                 int64_t begin, int64_t end, double dt, unsigned long long* out) {
+    double m = 0.0;
+    for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        rec4 a = q[i];
+        const rec4 b = p[i];
+        a.x = __dadd_rn(a.x, __dmul_rn(b.x, dt));
+        a.y = __dadd_rn(a.y, __dmul_rn(b.y, dt));
+        a.z = __dadd_rn(a.z, __dmul_rn(b.z, dt));
+        q[i] = a;
+        const rec4 r = q_ref[i];
+        double dx = __dsub_rn(a.x, r.x), dy = __dsub_rn(a.y, r.y), dz = __dsub_rn(a.z, r.z);
+        m = fmax(m, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz))));
     }
     m = block_max(m);
     if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
@@ -283,6 +307,16 @@ cudaError_t launch_unpack(const double* in, double* xyz, int64_t n, cudaStream_t
 cudaError_t launch_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, cudaStream_t s) {
     if (end <= begin) return cudaSuccess;
     k_integrate<<<grid_for(end - begin, kThreads), kThreads, 0, s>>>((rec4*)q, (const rec4*)p, begin, end, dt);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_integrate_disp(double* q, const double* p, const double* q_ref, int64_t begin, int64_t end,
+                                  double dt, double* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+    if (e != cudaSuccess || end <= begin) return e;
+    k_integrate_disp<<<grid_for(end - begin, kThreads, 148 * 8), kThreads, 0, s>>>(
+        (rec4*)q, (const rec4*)p, (const rec4*)q_ref, begin, end, dt, (unsigned long long*)out);
     g_launches++;
     return cudaGetLastError();
 }

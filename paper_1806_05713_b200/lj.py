@@ -26,7 +26,7 @@ EXPORTS = (
     "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_rebuild",
     "lj_cell_order",
     "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_force_step_variant", "lj_gather_probe",
-    "lj_list_interior", "lj_integrate",
+    "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
     "lj_wrap",
     "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
     "lj_version",
@@ -78,6 +78,7 @@ def load() -> ctypes.CDLL:
         "lj_list_interior": (st, [i64, i64, vp, vp, vp, vp, vp]),
         "lj_list_partner_ranges": (st, [i64, i64, vp, vp, vp, vp, i32, vp, vp]),
         "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
+        "lj_integrate_displacement": (st, [vp, vp, vp, i64, i64, d, vp, vp]),
         "lj_wrap": (st, [vp, vp, i64, d, vp]),
         "lj_max_displacement": (st, [vp, vp, i64, i64, vp, vp]),
         "lj_energy": (st, [vp, vp, i64, Geom, i64, i64, vp, vp, vp, i32, vp, vp]),
@@ -337,6 +338,16 @@ def integrate(q: torch.Tensor, p: torch.Tensor, dt: float, begin: int = 0, end: 
     _rec(p, "p")
     _check(load().lj_integrate(_ptr(q), _ptr(p), int(begin), q.shape[0] if end is None else int(end), float(dt),
                                _stream()))
+
+
+def integrate_displacement(q: torch.Tensor, p: torch.Tensor, q_ref: torch.Tensor, dt: float, begin: int, end: int,
+                           out: torch.Tensor) -> None:
+    """q += p dt on rows [begin, end) and out = max |q - q_ref| there, in one pass."""
+    _rec(q, "q")
+    _rec(p, "p")
+    _rec(q_ref, "q_ref")
+    _check(load().lj_integrate_displacement(_ptr(q), _ptr(p), _ptr(q_ref), int(begin), int(end), float(dt), _ptr(out),
+                                            _stream()))
 
 
 def wrap(q: torch.Tensor, L: float, q_ref: torch.Tensor | None = None) -> None:

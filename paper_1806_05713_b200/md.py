@@ -95,6 +95,10 @@ class LibBackend:
     def max_disp(self, q, q_ref, b, e, out):
         lj.max_displacement(q, q_ref, b, e, out)
 
+    def integrate_disp(self, q, p, q_ref, dt, b, e, out):
+        """integrate + max_disp in one pass (lj_integrate_displacement)."""
+        lj.integrate_displacement(q, p, q_ref, dt, b, e, out)
+
     def wrap(self, q, q_ref):
         lj.wrap(q, self.g.L, q_ref)
 
@@ -317,8 +321,11 @@ class LeapfrogMD:
         """q += p dt on own rows, the bookkeeping check (displacement all-reduce
         MAX first), then the position exchange: a blocking all-gather + rebuild
         when the list expires, else the all-gather (asynchronous with overlap)."""
-        self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
-        self.be.max_disp(self.q, self.q_ref, self.rb, self.re, self.disp)
+        if hasattr(self.be, "integrate_disp"):
+            self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, self.rb, self.re, self.disp)
+        else:
+            self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
+            self.be.max_disp(self.q, self.q_ref, self.rb, self.re, self.disp)
         self._allreduce_max(self.disp)
         if 2.0 * float(self.disp.item()) >= self.margin:
             self._allgather_q()

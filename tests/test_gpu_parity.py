@@ -550,3 +550,20 @@ def test_list_partner_ranges(lj, dev, systems, P, r):
     for s in range(P):
         m = j[(j >= bounds[s]) & (j < bounds[s + 1])]
         assert got[s] == ((int(m.min()), int(m.max())) if len(m) else None)
+
+
+@pytest.mark.parametrize("rows", [(0, 4000), (123, 3456)])
+def test_integrate_displacement_fused(lj, dev, systems, rows):
+    """lj_integrate_displacement == lj_integrate + lj_max_displacement, bit for bit."""
+    w = systems[1]
+    rb, re_ = rows
+    rng = np.random.default_rng(81)
+    q0 = to_dev(w.q, dev)
+    p = to_dev(rng.normal(0, 1, (w.n, 3)), dev)
+    qref = to_dev(w.q + rng.uniform(-0.05, 0.05, w.q.shape), dev)
+    qa, qb = q0.clone(), q0.clone()
+    lj.integrate(qa, p, 0.01, rb, re_)
+    da = lj.max_displacement(qa, qref, rb, re_)
+    db = torch.full((1,), 5.0, dtype=torch.float64, device=dev)
+    lj.integrate_displacement(qb, p, qref, 0.01, rb, re_, db)
+    assert torch.equal(qa, qb) and float(da.item()) == float(db.item())
