@@ -578,6 +578,27 @@ constexpr int kMaxRows = 256;   // atoms per cell handled by v4 (more -> overflo
 constexpr int kItemRows = 4;    // rows per work item
 constexpr int kMaxItems = kMaxRows / kItemRows + 8;
 
+__device__ __forceinline__ unsigned long long pack_f32x2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+
+// r2 = (dx*dx + dy*dy) + dz*dz as fmaf(dz, dz, fmaf(dy, dy, dx * dx)) for two
+// candidates at once (sm_100 packed fp32x2: FADD2 / FMUL2 / FFMA2).
+__device__ __forceinline__ void dist2_f32x2(unsigned long long cx, unsigned long long cy, unsigned long long cz,
+                                            const float4& ri, float& r2a, float& r2b) {
+    const unsigned long long rx = pack_f32x2(ri.x, ri.x), ry = pack_f32x2(ri.y, ri.y), rz = pack_f32x2(ri.z, ri.z);
+    unsigned long long dx, dy, dz, r2;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(cx), "l"(rx));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(cy), "l"(ry));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dz) : "l"(cz), "l"(rz));
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r2) : "l"(dx));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r2) : "l"(dy), "l"(r2));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r2) : "l"(dz), "l"(r2));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r2a), "=f"(r2b) : "l"(r2));
+}
+
 // Rank, in ascending wrapped coordinate, of the neighbour at offset d in {-1,0,1}
 // of cell coordinate v (nc >= 3, so the three wrapped values are distinct).
 __device__ __forceinline__ int axis_rank(int v, int d, int nc) {
@@ -833,16 +854,16 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
             for (int k0 = 0; k0 < len; k0 += 64) {
                 const float4 c0 = C[lst[k0 + lane]], c1 = C[lst[k0 + 32 + lane]];
                 const int j0 = __float_as_int(c0.w), j1 = __float_as_int(c1.w);
+                // the two candidates side by side in packed fp32x2 registers (FADD2/FFMA2,
+                // row coordinate broadcast): same IEEE operations as the scalar form
+                const unsigned long long cx = pack_f32x2(c0.x, c1.x), cy = pack_f32x2(c0.y, c1.y),
+                                         cz = pack_f32x2(c0.z, c1.z);
 #pragma unroll
                 for (int r = 0; r < kItemRows; r++) {
                     if (r >= nr) break;
                     const int i = __float_as_int(ri[r].w);
-                    float dx = c0.x - ri[r].x, dy = c0.y - ri[r].y, dz = c0.z - ri[r].z;
-                    const float r2a = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                    dx = c1.x - ri[r].x;
-                    dy = c1.y - ri[r].y;
-                    dz = c1.z - ri[r].z;
-                    const float r2b = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                    float r2a, r2b;
+                    dist2_f32x2(cx, cy, cz, ri[r], r2a, r2b);
                     bool acc0 = r2a < a.lo2, acc1 = r2b < a.lo2;
                     const bool band0 = !acc0 && r2a < a.hi2, band1 = !acc1 && r2b < a.hi2;
                     if (__any_sync(0xffffffffu, band0 | band1)) {   // rare: the oracle's exact test
