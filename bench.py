@@ -358,15 +358,42 @@ def main():
         sim.interactions()
         barrier()
         torch.cuda.synchronize()
+        # every step: H2D of the own rows of q and p from pinned host memory, the step,
+        # D2H of both.  Copies run on two copy streams so that opposite directions
+        # overlap (H2D p(k+1) with D2H q(k); D2H p(k) with the drift/exchange of step k).
+        ci, co = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_pout = ev_qout = None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        ci.wait_stream(stream)
+        co.wait_stream(stream)
         for _ in range(args.steps):
             sim.sync_positions()
-            sim.q[rb:re_].copy_(qh, non_blocking=True)
-            sim.p[rb:re_].copy_(ph, non_blocking=True)
-            one_step(False)
-            qh.copy_(sim.q[rb:re_], non_blocking=True)
-            ph.copy_(sim.p[rb:re_], non_blocking=True)
+            qd, pd = sim.q, sim.p
+            with torch.cuda.stream(ci):
+                if ev_pout is not None:
+                    ci.wait_event(ev_pout)
+                pd[rb:re_].copy_(ph, non_blocking=True)
+                ev_pin = ci.record_event()
+                if ev_qout is not None:
+                    ci.wait_event(ev_qout)
+                qd[rb:re_].copy_(qh, non_blocking=True)
+                ev_qin = ci.record_event()
+            stream.wait_event(ev_pin)
+            stream.wait_event(ev_qin)
+            sim.kick(w.dt, sim.counter)
+            co.wait_event(stream.record_event())
+            with torch.cuda.stream(co):
+                ph.copy_(pd[rb:re_], non_blocking=True)   # p is final after the kick (unless re-sorted)
+            sim.drift_and_exchange()
+            co.wait_event(stream.record_event())
+            with torch.cuda.stream(co):
+                if sim.p is not pd:                        # a rebuild re-sorted the atoms: p again
+                    ph.copy_(sim.p[rb:re_], non_blocking=True)
+                ev_pout = co.record_event()
+                qh.copy_(sim.q[rb:re_], non_blocking=True)
+                ev_qout = co.record_event()
+        stream.wait_event(ev_qout)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -401,7 +428,8 @@ def main():
                        "exchange": (("halo" if sim.halo else "all-gather")
                                     + (" (async, overlapped with the interior rows' force)" if sim.overlap else "")
                                     if (world > 1 or sim.collective) else "none (1 rank)"),
-                       "l2": "inputs larger than L2 (CSR list %.2f GB + records)" % (4 * sim.lst.n_entries / 1e9),
+                       "l2": "inputs larger than L2 (list %.2f GB of entries in a %.2f GB padded array + %.0f MB of records)"
+                             % (4 * sim.lst.n_entries / 1e9, 4 * sim.lst.sorted_list.numel() / 1e9, 64 * w.n / 1e6),
                        "rebuilds_in_timed_steps": rebuilds},
             "ms_per_force_step": force_avg,
             "roofline": roof,
