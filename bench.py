@@ -381,11 +381,15 @@ def main():
                 ev_qin = ci.record_event()
             stream.wait_event(ev_pin)
             stream.wait_event(ev_qin)
-            sim.kick(w.dt, sim.counter)
+            if force_only:   # configs 2/3: the force step alone, as the timed loop
+                be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
+            else:
+                sim.kick(w.dt, sim.counter)
             co.wait_event(stream.record_event())
             with torch.cuda.stream(co):
                 ph.copy_(pd[rb:re_], non_blocking=True)   # p is final after the kick (unless re-sorted)
-            sim.drift_and_exchange()
+            if not force_only:
+                sim.drift_and_exchange()
             co.wait_event(stream.record_event())
             with torch.cuda.stream(co):
                 if sim.p is not pd:                        # a rebuild re-sorted the atoms: p again
