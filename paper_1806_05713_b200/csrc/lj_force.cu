@@ -48,11 +48,8 @@ __device__ __forceinline__ double fast_rcp(double x) {
     return fma(y, fma(e, e, e), y);
 }
 
-// |d| > L/2 (up to the low word; pairs that close to L/2 are never neighbours)
-__device__ __forceinline__ bool beyond_half(double d, int hi_halfL) {
-    return (__double2hiint(d) & 0x7fffffff) > hi_halfL;
-}
-
+// Periodic image shift of a raw difference: +-L when |d| > L/2 (decided on the
+// high words, up to the low word -- pairs that close to L/2 are never within r_c).
 __device__ __forceinline__ double image_shift(double d, double L, int hi_halfL) {
     int hi = __double2hiint(d);
     double s = ((hi & 0x7fffffff) > hi_halfL) ? L : 0.0;

@@ -278,8 +278,7 @@ struct ListArgs {
     int64_t ncell;
     CellGrid cg;
     double rs2;               // rs*rs, the oracle's constant
-    float rs2_screen;         // conservative fp32 screen radius^2 (> rs2 + max fp32 error)
-    float r_screen;           // >= sqrt(rs2_screen): reach of a row for the half-cell type lists
+    float r_screen;           // reach of a row for the v3 half-cell type lists (> rs + max fp32 error)
     int half;
     int64_t row_begin, row_end;
     int32_t* npart;           // [rows]
@@ -1215,7 +1214,6 @@ static ListArgs list_args(const double* q, const CellGrid& cg, double rs, int ha
     // fp32 screen: positions (|x| <= L) carry <= ~2 ulp(L) = 2.4e-7 L error per axis;
     // widen the radius by 8e-7 L + 1e-5 so every exact pair passes the screen.
     double rsc = rs + 8e-7 * cg.L + 1e-5;
-    a.rs2_screen = (float)(rsc * rsc);
     a.r_screen = (float)(rsc * (1.0 + 1e-5));
     a.half = half;
     a.row_begin = row_begin;
