@@ -333,7 +333,7 @@ def main():
                 "achieved": gather_bytes / (force_avg * 1e-3) / 1e9,
                 "peak": gather_bytes / (floor_ms * 1e-3) / 1e9,
                 "unit": "GB/s", "frac": floor_ms / force_avg, "traffic": traffic,
-                "kernel": "k_force (full list, 4 lanes per row)",
+                "kernel": "k_force (full list, 4 lanes per row, 3 gathers in flight per lane)",
                 "definition": "BASELINE.json north_star: slower of partner-gather bytes at achieved L2/HBM "
                               "bandwidth (lj_gather_probe, same list and lanes, measured live) and FP64 at peak",
                 "bytes_per_entry": BYTES_PER_ENTRY, "bytes_per_row": BYTES_PER_ROW, "entries_per_launch": E,

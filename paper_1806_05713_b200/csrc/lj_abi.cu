@@ -275,15 +275,16 @@ lj_status lj_force_step_ex(const double* q, double* p, int64_t n, lj_geom g, dou
         return fail(LJ_ERR_ARG, "force: null pointer");
     if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "force: q/p not 32-byte aligned");
     int lanes = lanes_per_row & 0xff, unroll = lanes_per_row >> 8;
-    if (lanes == 0) {   // defaults from the round-1 sweeps (profiles/r01_sweep_*.jsonl)
+    if (lanes == 0) {   // defaults from the round-1 sweeps (profiles/r01_sweep_*.jsonl, tools/gu_sweep.py)
         const int64_t rows_ = row_end - row_begin;
-        lanes = (!half && rows_ >= 500000) ? 4 : 8;
-        if (unroll == 0) unroll = 2;
+        const bool big = !half && rows_ >= 500000;
+        lanes = big ? 4 : 8;
+        if (unroll == 0) unroll = big ? 3 : 2;   // config 4: G4/U3 0.766 ms, G4/U2 0.783 ms
     }
     if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
         return fail(LJ_ERR_ARG, "force: lanes_per_row must be 0,1,2,4,8,16 or 32 (got %d)", lanes_per_row);
-    if (unroll != 0 && unroll != 2 && unroll != 4)
-        return fail(LJ_ERR_ARG, "force: unroll (lanes_per_row >> 8) must be 0, 2 or 4 (got %d)", unroll);
+    if (unroll != 0 && unroll != 2 && unroll != 3 && unroll != 4)
+        return fail(LJ_ERR_ARG, "force: unroll (lanes_per_row >> 8) must be 0, 2, 3 or 4 (got %d)", unroll);
     lanes |= unroll << 8;
     ForceArgs a;
     a.q = q;

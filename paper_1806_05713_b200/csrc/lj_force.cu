@@ -85,7 +85,7 @@ __device__ __forceinline__ void count_interactions(unsigned cnt, unsigned long l
 // U = 2: at most 48 registers -> 5 CTAs (40 warps) per SM; measured 0.79 vs 0.83 ms
 // (54 registers, 4 CTAs) on config 4 -- the kernel is latency/L1-bound, warps help.
 template <int G, int U, bool HALF>
-__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : 3)
+__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
     k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
             const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
             PairConsts c, unsigned long long* n_inter) {
@@ -435,6 +435,7 @@ cudaError_t launch_gu(const ForceArgs& a, int lanes, cudaStream_t s) {
     const int U = lanes >> 8;
     const int G = lanes & 0xff;
     if (U == 4) return launch_g<HALF, 4>(a, G, s);
+    if (U == 3) return launch_g<HALF, 3>(a, G, s);
     if (U == 0 || U == 2) return launch_g<HALF, 2>(a, G, s);
     return cudaErrorInvalidValue;
 }

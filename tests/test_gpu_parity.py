@@ -182,7 +182,7 @@ def oracle_force(w, p0, half):
 
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 @pytest.mark.parametrize("half", [True, False])
-@pytest.mark.parametrize("lanes", [0, 1, 4, 8, 16, 32, 4 | 1024, 16 | 1024])
+@pytest.mark.parametrize("lanes", [0, 1, 4, 8, 16, 32, 4 | 768, 4 | 1024, 16 | 1024])
 def test_force_parity(lj, dev, systems, cfg, half, lanes):
     w = systems[cfg]
     rng = np.random.default_rng(cfg)
