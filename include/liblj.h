@@ -186,10 +186,11 @@ lj_status lj_force_step_variant(int layout, int rcp, const double *q, double *p,
                                 unsigned long long *n_interactions, void *stream);
 
 /* Roofline probe (not part of the method): the memory traffic of lj_force_step
- * on a full list -- the same lanes-per-row mapping, index loads and 256-bit
- * record gathers -- with no arithmetic beyond a running sum written to *sink
- * (device double).  Its duration is the gather-bandwidth floor of the force
- * kernel (SURVEY §8(d) "gather-only replay of the actual CSR list"). */
+ * on a full list -- the same lanes-per-row mapping and gathers in flight
+ * (lanes_per_row = G | (U << 8) as lj_force_step_ex, 0 = its defaults), index
+ * loads and 256-bit record gathers -- with no arithmetic beyond a running sum
+ * written to *sink (device double).  Its duration is the gather-bandwidth floor
+ * of the force kernel (SURVEY §8(d) "gather-only replay of the actual CSR list"). */
 lj_status lj_gather_probe(const double *q, int64_t n, int64_t row_begin, int64_t row_end,
                           const int32_t *number_of_partners, const int64_t *pointer,
                           const int32_t *sorted_list, int lanes_per_row, double *sink, void *stream);

@@ -356,9 +356,14 @@ lj_status lj_gather_probe(const double* q, int64_t n, int64_t row_begin, int64_t
     if (!sink || (row_end > row_begin && (!q || !number_of_partners || !pointer)))
         return fail(LJ_ERR_ARG, "gather_probe: null pointer");
     if (!aligned32(q)) return fail(LJ_ERR_ARG, "gather_probe: q not 32-byte aligned");
-    int lanes = lanes_per_row == 0 ? ((row_end - row_begin) >= 500000 ? 4 : 8) : lanes_per_row;
-    if (lanes != 4 && lanes != 8 && lanes != 16)
-        return fail(LJ_ERR_ARG, "gather_probe: lanes_per_row must be 0, 4, 8 or 16 (got %d)", lanes_per_row);
+    // same encoding and defaults as lj_force_step_ex on a full list: G | (U << 8)
+    const bool big = (row_end - row_begin) >= 500000;
+    int lanes = lanes_per_row & 0xff, unroll = lanes_per_row >> 8;
+    if (lanes == 0) lanes = big ? 4 : 8;
+    if (unroll == 0) unroll = (big && (lanes_per_row & 0xff) == 0) ? 3 : 2;
+    if (!((lanes == 4 || lanes == 8) && (unroll == 2 || unroll == 3)) && !(lanes == 16 && unroll == 2))
+        return fail(LJ_ERR_ARG, "gather_probe: unsupported lanes_per_row 0x%x", lanes_per_row);
+    lanes |= unroll << 8;
     ForceArgs a;
     a.q = q;
     a.p = nullptr;

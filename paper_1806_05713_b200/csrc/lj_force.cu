@@ -304,30 +304,39 @@ __global__ void __launch_bounds__(kForceThreads, (LAYOUT == LJ_LAYOUT_SOA || LAY
     count_interactions(cnt, n_inter);
 }
 
-// Roofline probe: the force kernel's access pattern (G lanes per row, two
-// gathers in flight, next indices prefetched) without the arithmetic.
-template <int G>
-__global__ void __launch_bounds__(kForceThreads)
+// Roofline probe: the force kernel's access pattern (G lanes per row, U gathers
+// in flight per lane, next indices prefetched, the same warp-uniform chunk loop)
+// without the arithmetic.
+template <int G, int U>
+__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
     k_gather_probe(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
                    const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* sink) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t r = t / G;
     const int g = threadIdx.x % G;
+    const bool active = r < rows;
+    const int64_t i = active ? r : 0;
+    const int32_t* __restrict__ lst = list + (active ? ptr[r] : 0);
+    const int n = active ? npart[r] : 0;
     double s = 0.0;
-    if (r < rows) {
-        const int32_t* __restrict__ lst = list + ptr[r];
-        const int n = npart[r];
-        int jn0 = g < n ? __ldg(lst + g) : -1, jn1 = g + G < n ? __ldg(lst + g + G) : -1;
-        for (int k0 = g; k0 < n; k0 += 2 * G) {
-            const int j0 = jn0, j1 = jn1;
-            rec4 a, b;
-            if (j0 >= 0) a = load_rec(q, j0);
-            if (j1 >= 0) b = load_rec(q, j1);
-            jn0 = k0 + 2 * G < n ? __ldg(lst + k0 + 2 * G) : -1;
-            jn1 = k0 + 3 * G < n ? __ldg(lst + k0 + 3 * G) : -1;
-            if (j0 >= 0) s += a.x + a.y + a.z;
-            if (j1 >= 0) s += b.x + b.y + b.z;
+    int jn[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
+    for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
+        rec4 qj[U];
+        int j[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            j[u] = jn[u];
+            qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);
         }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int kn = k0 + U * G + u * G;
+            jn[u] = kn < n ? __ldg(lst + kn) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) s += j[u] >= 0 ? qj[u].x + qj[u].y + qj[u].z : 0.0;
     }
     if (s == 1.2345678e300) sink[0] = s;   // never true: keeps the loads alive
 }
@@ -445,14 +454,18 @@ cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s) { r
 
 cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cudaStream_t s) {
     if (a.rows <= 0) return cudaSuccess;
-    const unsigned grid = (unsigned)((a.rows * (int64_t)lanes + kForceThreads - 1) / kForceThreads);
+    const unsigned grid = (unsigned)((a.rows * (int64_t)(lanes & 0xff) + kForceThreads - 1) / kForceThreads);
     const rec4* q = (const rec4*)a.q;
+#define LJ_PROBE(G, U) k_gather_probe<G, U><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink)
     switch (lanes) {
-        case 4: k_gather_probe<4><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink); break;
-        case 8: k_gather_probe<8><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink); break;
-        case 16: k_gather_probe<16><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink); break;
+        case 4 | (2 << 8): LJ_PROBE(4, 2); break;
+        case 4 | (3 << 8): LJ_PROBE(4, 3); break;
+        case 8 | (2 << 8): LJ_PROBE(8, 2); break;
+        case 8 | (3 << 8): LJ_PROBE(8, 3); break;
+        case 16 | (2 << 8): LJ_PROBE(16, 2); break;
         default: return cudaErrorInvalidValue;
     }
+#undef LJ_PROBE
     g_launches++;
     return cudaGetLastError();
 }
