@@ -80,6 +80,45 @@ def test_validation_before_launch(L):
     assert L.lj_wrap(None, None, 0, 0.0, None) == lj.LJ_ERR_ARG
 
 
+def test_validation_of_the_step_entry_points(L):
+    """Host-side argument checks of lj_rebuild, the ablation / probe / overlap /
+    halo entry points: all return before any device work, so they run here."""
+    g = lj.Geom(15.874011, 3.0, 3.3)
+    a, b, c, d = (ctypes.c_void_p(256 * k) for k in (1, 2, 3, 4))
+    ne = ctypes.c_int64()
+    # rebuild: q_out aliasing q, then p without p_out
+    st = L.lj_rebuild(a, b, a, c, None, d, 100, g, 0, 0, 100, 0, a, b, c, 1 << 20, ctypes.byref(ne), d, 1 << 20,
+                      None)
+    assert st == lj.LJ_ERR_ARG and b"distinct" in L.lj_last_error()
+    st = L.lj_rebuild(a, b, c, None, None, d, 100, g, 0, 0, 100, 0, a, b, c, 1 << 20, ctypes.byref(ne), d, 1 << 20,
+                      None)
+    assert st == lj.LJ_ERR_ARG
+    # variant: layout / reciprocal / lanes out of range
+    for layout, rcp, lanes, word in ((4, 0, 4, b"layout"), (0, 4, 4, b"reciprocal"), (0, 0, 2, b"lanes")):
+        st = L.lj_force_step_variant(layout, rcp, a, b, 10, g, 0.01, 0, 10, a, b, c, lanes, None, None)
+        assert st == lj.LJ_ERR_ARG and word in L.lj_last_error()
+    # probe: misaligned q, unsupported G|U
+    st = L.lj_gather_probe(ctypes.c_void_p(264), 10, 0, 10, a, b, c, 0, d, None)
+    assert st == lj.LJ_ERR_ARG and b"aligned" in L.lj_last_error()
+    st = L.lj_gather_probe(a, 10, 0, 10, a, b, c, 32 | (2 << 8), d, None)
+    assert st == lj.LJ_ERR_ARG and b"lanes" in L.lj_last_error()
+    # interior / partner ranges: bad ranges, P out of [1, 64], null pointers
+    assert L.lj_list_interior(5, 4, a, b, c, d, None) == lj.LJ_ERR_ARG
+    assert L.lj_list_interior(0, 4, None, b, c, d, None) == lj.LJ_ERR_ARG
+    for P in (0, 65):
+        st = L.lj_list_partner_ranges(0, 4, a, b, c, d, P, a, None)
+        assert st == lj.LJ_ERR_ARG and b"P" in L.lj_last_error()
+    assert L.lj_list_partner_ranges(0, 4, a, b, c, None, 2, a, None) == lj.LJ_ERR_ARG
+    # fused drift + displacement: null max_disp, misaligned q_ref, nan dt, bad range
+    assert L.lj_integrate_displacement(a, b, c, 0, 10, 0.01, None, None) == lj.LJ_ERR_ARG
+    st = L.lj_integrate_displacement(a, b, ctypes.c_void_p(264), 0, 10, 0.01, d, None)
+    assert st == lj.LJ_ERR_ARG and b"aligned" in L.lj_last_error()
+    assert L.lj_integrate_displacement(a, b, c, 0, 10, float("inf"), d, None) == lj.LJ_ERR_ARG
+    assert L.lj_integrate_displacement(a, b, c, 10, 0, 0.01, d, None) == lj.LJ_ERR_ARG
+    # nothing above reached the device
+    assert L.lj_launch_count() == 0
+
+
 def test_product_binding_has_no_cpu_fallback():
     """The product package never imports the oracle or a CPU path."""
     pkg = os.path.join(ROOT, "paper_1806_05713_b200")
