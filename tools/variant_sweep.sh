@@ -1,0 +1,7 @@
+# time the list build of config 4 for every prebuilt library variant in variants/ (development tool)
+cp paper_1806_05713_b200/liblj.so /tmp/liblj_default.so
+for f in variants/*.so; do
+  cp $f paper_1806_05713_b200/liblj.so
+  echo "variant=$f"; python tools/build_time.py ${CFG:-4} 2>&1 | grep '"padded": true'
+done
+cp /tmp/liblj_default.so paper_1806_05713_b200/liblj.so
