@@ -371,10 +371,15 @@ def main():
     # ---- e2e: same steps through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        qh = torch.empty((re_ - rb, 4), dtype=torch.float64, pin_memory=True)
-        ph = torch.empty((re_ - rb, 4), dtype=torch.float64, pin_memory=True)
-        qh.copy_(sim.q[rb:re_])
-        ph.copy_(sim.p[rb:re_])
+        # host side: the user's (n, 3) position / momentum arrays in pinned memory;
+        # the device packs them into the AoS4 records (lj_pack_aos4) and unpacks the
+        # result (lj_unpack_aos4), so 24 B per atom and array cross PCIe, not 32
+        nl = re_ - rb
+        qh = torch.empty((nl, 3), dtype=torch.float64, pin_memory=True)
+        ph = torch.empty((nl, 3), dtype=torch.float64, pin_memory=True)
+        qh.copy_(sim.q[rb:re_, :3])
+        ph.copy_(sim.p[rb:re_, :3])
+        q_in, p_in, q_out, p_out, p_out2 = (torch.empty((nl, 3), dtype=torch.float64, device=dev) for _ in range(5))
         sim.interactions()
         barrier()
         torch.cuda.synchronize()
@@ -393,29 +398,35 @@ def main():
             with torch.cuda.stream(ci):
                 if ev_pout is not None:
                     ci.wait_event(ev_pout)
-                pd[rb:re_].copy_(ph, non_blocking=True)
+                p_in.copy_(ph, non_blocking=True)
                 ev_pin = ci.record_event()
                 if ev_qout is not None:
                     ci.wait_event(ev_qout)
-                qd[rb:re_].copy_(qh, non_blocking=True)
+                q_in.copy_(qh, non_blocking=True)
                 ev_qin = ci.record_event()
             stream.wait_event(ev_pin)
+            lj.pack_aos4(p_in, out=pd[rb:re_])
             stream.wait_event(ev_qin)
+            lj.pack_aos4(q_in, out=qd[rb:re_])
             if force_only:   # configs 2/3: the force step alone, as the timed loop
                 be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
             else:
                 sim.kick(w.dt, sim.counter)
+            lj.unpack_aos4(pd[rb:re_], out=p_out)
             co.wait_event(stream.record_event())
             with torch.cuda.stream(co):
-                ph.copy_(pd[rb:re_], non_blocking=True)   # p is final after the kick (unless re-sorted)
+                ph.copy_(p_out, non_blocking=True)   # p is final after the kick (unless re-sorted)
             if not force_only:
                 sim.drift_and_exchange()
+            if sim.p is not pd:                       # a rebuild re-sorted the atoms: p again
+                lj.unpack_aos4(sim.p[rb:re_], out=p_out2)
+            lj.unpack_aos4(sim.q[rb:re_], out=q_out)
             co.wait_event(stream.record_event())
             with torch.cuda.stream(co):
-                if sim.p is not pd:                        # a rebuild re-sorted the atoms: p again
-                    ph.copy_(sim.p[rb:re_], non_blocking=True)
+                if sim.p is not pd:
+                    ph.copy_(p_out2, non_blocking=True)
                 ev_pout = co.record_event()
-                qh.copy_(sim.q[rb:re_], non_blocking=True)
+                qh.copy_(q_out, non_blocking=True)
                 ev_qout = co.record_event()
         stream.wait_event(ev_qout)
         e1.record(stream)
@@ -426,7 +437,7 @@ def main():
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e_pairs = sim.interactions()
         e_pairs = e_pairs if half else e_pairs / 2.0
-        nbytes = 2 * (re_ - rb) * 32
+        nbytes = 2 * (re_ - rb) * 24
         e2e = {"value": e_pairs / (float(ems.item()) * 1e-3) / 1e9, "unit": "G pair-interactions/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "ms_per_step": float(ems.item()) / args.steps}

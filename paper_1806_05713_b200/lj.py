@@ -141,9 +141,13 @@ def pack_aos4(xyz: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tenso
     return out
 
 
-def unpack_aos4(q: torch.Tensor) -> torch.Tensor:
+def unpack_aos4(q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(n,4) AoS4 records -> (n,3) float64 (into `out` if given: contiguous, same device)."""
     _rec(q, "q")
-    out = torch.empty((q.shape[0], 3), dtype=torch.float64, device=q.device)
+    if out is None:
+        out = torch.empty((q.shape[0], 3), dtype=torch.float64, device=q.device)
+    elif not (out.is_cuda and out.dtype == torch.float64 and out.is_contiguous() and out.shape == (q.shape[0], 3)):
+        raise TypeError("unpack_aos4: out must be a contiguous CUDA float64 (n,3) tensor")
     _check(load().lj_unpack_aos4(_ptr(q), _ptr(out), q.shape[0], _stream()))
     return out
 
