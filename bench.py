@@ -71,7 +71,7 @@ def peaks():
 
 class ClockSampler:
     def __init__(self, index):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.power_w, self.reasons, self.max_mhz = [], [], set(), None
         self._stop = threading.Event()
         self._t = None
         try:
@@ -101,6 +101,10 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:  # noqa: BLE001
                 pass
+            try:
+                self.power_w.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+            except Exception:  # noqa: BLE001
+                pass
             time.sleep(0.005)
 
     def start(self):
@@ -114,8 +118,11 @@ class ClockSampler:
             self._t.join()
         if not self.samples:
             return None
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power_w:
+            out["power_w"] = statistics.median(self.power_w)
+        return out
 
 
 # ---- the oracle as the CPU baseline / reference arm ---------------------------------

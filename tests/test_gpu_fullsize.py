@@ -92,3 +92,36 @@ def test_fullsize_half_list_sampled(lj):
         rows = gl.sorted_list[a * stride:e * stride].view(e - a, stride).cpu().numpy()
         for r in range(a, e):
             assert np.array_equal(rows[r - a, :npart[r]], ol.row(r - a)), f"row {r}"
+
+
+def test_fullsize_snapshot_parity_after_md_rebuild(lj):
+    """SURVEY Pin-13 on the bench path: config 4 through the product MD driver
+    (leapfrog kick + drift + bookkeeping, fused lj_rebuild re-sorting into cell
+    order) until the list has been rebuilt on evolved positions; the oracle then
+    builds sampled rows from that GPU snapshot of q and the pair sets must be
+    identical; the permutation carried in p's pad lane stays a permutation."""
+    from paper_1806_05713_b200 import md
+    dev = torch.device("cuda:0")
+    w = lj_inputs.config(4)
+    g = lj.geom(w.L, w.rc, w.rs)
+    sim = md.LeapfrogMD(md.LibBackend(w.n, g, 0, w.n, dev), w.q, w.p, g, w.dt, reorder=True)
+    for _ in range(12):
+        sim.kick(w.dt)
+        sim.drift_and_exchange()
+        if sim.stats.rebuilds >= 1:
+            break
+    assert sim.stats.rebuilds >= 1, "no bookkeeping rebuild within 12 steps"
+    torch.cuda.synchronize()
+    qs = np.ascontiguousarray(sim.q[:, :3].cpu().numpy())
+    assert qs.min() >= 0.0 and qs.max() < w.L        # wrapped at the rebuild
+    ids = np.sort(sim.atom_ids().cpu().numpy())
+    assert np.array_equal(ids, np.arange(w.n))
+    lst = sim.lst
+    stride = lj.LJ_PADDED_ROW_STRIDE
+    npart = lst.number_of_partners.cpu().numpy()
+    for (a, e) in _windows(w.n, 13):
+        ol = oracle.list_cells(qs, w.L, w.rs, False, a, e)
+        assert np.array_equal(npart[a:e], ol.number_of_partners)
+        rows = lst.sorted_list[a * stride:e * stride].view(e - a, stride).cpu().numpy()
+        for r in range(a, e):
+            assert np.array_equal(rows[r - a, :npart[r]], ol.row(r - a)), f"row {r}"
