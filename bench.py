@@ -264,7 +264,7 @@ def main():
         sim.drift_and_exchange()          # integrate, displacement check, all-gather / rebuild
         return e
 
-    every = args.energy_every if args.energy_every is not None else (max(1, args.steps // 20) if args.config == 5 else 0)
+    every = args.energy_every if args.energy_every is not None else (max(2, args.steps // 20) if args.config == 5 else 0)
     energies = []
 
     for _ in range(args.warmup):
@@ -380,8 +380,15 @@ def main():
     if not args.no_e2e:
         # host side: the user's (n, 3) position / momentum arrays in pinned memory;
         # the device packs them into the AoS4 records (lj_pack_aos4) and unpacks the
-        # result (lj_unpack_aos4), so 24 B per atom and array cross PCIe, not 32
+        # result (lj_unpack_aos4), so 24 B per atom and array cross PCIe, not 32.
+        # The own rows are streamed in K chunks: H2D and D2H run on two copy streams
+        # (PCIe is full duplex) and overlap the force on the other chunks; a chunk's
+        # H2D of step k+1 waits only for the same chunk's D2H of step k (the state
+        # round-trips through the host buffers every step).
         nl = re_ - rb
+        K = 4 if (nl >= 1 << 20 and not half) else 1   # small systems and half lists: one chunk
+        cb = [rb + (nl * c) // K for c in range(K + 1)]
+        cs = [slice(cb[c] - rb, cb[c + 1] - rb) for c in range(K)]
         qh = torch.empty((nl, 3), dtype=torch.float64, pin_memory=True)
         ph = torch.empty((nl, 3), dtype=torch.float64, pin_memory=True)
         qh.copy_(sim.q[rb:re_, :3])
@@ -390,52 +397,56 @@ def main():
         sim.interactions()
         barrier()
         torch.cuda.synchronize()
-        # every step: H2D of the own rows of q and p from pinned host memory, the step,
-        # D2H of both.  Copies run on two copy streams so that opposite directions
-        # overlap (H2D p(k+1) with D2H q(k); D2H p(k) with the drift/exchange of step k).
         ci, co = torch.cuda.Stream(), torch.cuda.Stream()
-        ev_pout = ev_qout = None
+        ev_pout, ev_qout = [None] * K, [None] * K
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ci.wait_stream(stream)
         co.wait_stream(stream)
-        for _ in range(args.steps):
-            sim.sync_positions()
-            qd, pd = sim.q, sim.p
+
+        def h2d(dst, src, c, after):
             with torch.cuda.stream(ci):
-                if ev_pout is not None:
-                    ci.wait_event(ev_pout)
-                p_in.copy_(ph, non_blocking=True)
-                ev_pin = ci.record_event()
-                if ev_qout is not None:
-                    ci.wait_event(ev_qout)
-                q_in.copy_(qh, non_blocking=True)
-                ev_qin = ci.record_event()
-            stream.wait_event(ev_pin)
-            lj.pack_aos4(p_in, out=pd[rb:re_])
-            stream.wait_event(ev_qin)
-            lj.pack_aos4(q_in, out=qd[rb:re_])
-            if force_only:   # configs 2/3: the force step alone, as the timed loop
-                be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
-            else:
-                sim.kick(w.dt, sim.counter)
-            lj.unpack_aos4(pd[rb:re_], out=p_out)
+                if after[c] is not None:
+                    ci.wait_event(after[c])
+                dst[cs[c]].copy_(src[cs[c]], non_blocking=True)
+                return ci.record_event()
+
+        def d2h(dst, src, c):
             co.wait_event(stream.record_event())
             with torch.cuda.stream(co):
-                ph.copy_(p_out, non_blocking=True)   # p is final after the kick (unless re-sorted)
+                dst[cs[c]].copy_(src[cs[c]], non_blocking=True)
+                return co.record_event()
+
+        resorts = 0
+        for _ in range(args.steps):
+            sim.sync_positions()                  # the exchange of the previous step (P > 1)
+            qd, pd = sim.q, sim.p
+            ev_q = [h2d(q_in, qh, c, ev_qout) for c in range(K)]
+            ev_p = [h2d(p_in, ph, c, ev_pout) for c in range(K)]
+            for c in range(K):
+                stream.wait_event(ev_q[c])
+                lj.pack_aos4(q_in[cs[c]], out=qd[cb[c]:cb[c + 1]])
+            for c in range(K):   # force per chunk as soon as its momenta have arrived
+                stream.wait_event(ev_p[c])
+                lj.pack_aos4(p_in[cs[c]], out=pd[cb[c]:cb[c + 1]])
+                if K == 1:
+                    be.force(sim.q, sim.p, w.dt, sim.lst, sim.counter)
+                else:
+                    be.force_rows(sim.q, sim.p, w.dt, sim.lst, cb[c], cb[c + 1], sim.counter)
+                lj.unpack_aos4(pd[cb[c]:cb[c + 1]], out=p_out[cs[c]])
+                ev_pout[c] = d2h(ph, p_out, c)   # p is final after the kick (unless re-sorted)
             if not force_only:
                 sim.drift_and_exchange()
-            if sim.p is not pd:                       # a rebuild re-sorted the atoms: p again
+            if sim.p is not pd:                   # a rebuild re-sorted the atoms: p again
+                resorts += 1
                 lj.unpack_aos4(sim.p[rb:re_], out=p_out2)
-            lj.unpack_aos4(sim.q[rb:re_], out=q_out)
-            co.wait_event(stream.record_event())
-            with torch.cuda.stream(co):
-                if sim.p is not pd:
-                    ph.copy_(p_out2, non_blocking=True)
-                ev_pout = co.record_event()
-                qh.copy_(q_out, non_blocking=True)
-                ev_qout = co.record_event()
-        stream.wait_event(ev_qout)
+                ev_pout = [d2h(ph, p_out2, c) for c in range(K)]
+            for c in range(K):
+                lj.unpack_aos4(sim.q[cb[c]:cb[c + 1]], out=q_out[cs[c]])
+                ev_qout[c] = d2h(qh, q_out, c)
+        for c in range(K):
+            stream.wait_event(ev_qout[c])
+            stream.wait_event(ev_pout[c])
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -446,7 +457,7 @@ def main():
         e_pairs = e_pairs if half else e_pairs / 2.0
         nbytes = 2 * (re_ - rb) * 24
         e2e = {"value": e_pairs / (float(ems.item()) * 1e-3) / 1e9, "unit": "G pair-interactions/s",
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + resorts * (re_ - rb) * 24 / args.steps,
                "ms_per_step": float(ems.item()) / args.steps}
 
     cpu = None
