@@ -51,8 +51,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="configs 2/3: launch every force step eagerly")
     ap.add_argument("--no-overlap", action="store_true", help="P > 1: blocking all-gather (no comm/compute overlap)")
-    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
-                    help="P > 1: position exchange between rebuilds (halo = only the rows each rank's list reads)")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo", "push"],
+                    help="P > 1: position exchange between rebuilds (halo = only the rows each rank's list reads, "
+                         "over NCCL send/recv; push = the same rows stored into the peers' replicas by the "
+                         "integrate kernel itself over CUDA IPC / NVLink)")
     ap.add_argument("--energy-every", type=int, default=None,
                     help="NVE energy sample interval in timed steps (default: config 5 -> steps/20, else off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -478,7 +480,7 @@ def main():
             "config": {"workload": f"config{args.config}", "n_atoms": w.n, "list": "half" if half else "full",
                        "order": order + (" (re-sorted at every rebuild)" if order == "cell" and not force_only else ""),
                        "dt": w.dt, "rc": w.rc, "rs": w.rs, "parallelism": f"rows/{world}",
-                       "exchange": (("halo" if sim.halo else "all-gather")
+                       "exchange": (("fused integrate + NVLink push" if sim.push else "halo" if sim.halo else "all-gather")
                                     + (" (async, overlapped with the interior rows' force)" if sim.overlap else "")
                                     if (world > 1 or sim.collective) else "none (1 rank)"),
                        "l2": "inputs larger than L2 (list %.2f GB of entries in a %.2f GB padded array + %.0f MB of records)"

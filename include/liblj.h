@@ -227,6 +227,46 @@ lj_status lj_integrate(double *q, const double *p, int64_t begin, int64_t end, d
 lj_status lj_integrate_displacement(double *q, const double *p, const double *q_ref, int64_t begin, int64_t end,
                                    double dt, double *max_disp, void *stream);
 
+/* ---- fused drift + NVLink push ------------------------ */
+
+/* One destination of lj_integrate_push: rows [lo, hi) of the caller's own range
+ * are also stored to dst (a q replica of another rank, n records, mapped into
+ * this process -- by lj_ipc_open on another GPU of the node, or any device
+ * pointer), at the same row index. */
+typedef struct {
+    double *dst;
+    int64_t lo, hi;
+} lj_push_target;
+
+#ifndef LJ_MAX_PUSH_TARGETS
+#define LJ_MAX_PUSH_TARGETS 63
+#endif
+
+/* lj_integrate_displacement with the position exchange fused in: for own rows
+ * [begin, end), q_out_i = q_in_i + p_i dt (bit-identical to lj_integrate),
+ * *max_disp = max |q_out_i - q_ref_i| (as lj_max_displacement), and every
+ * updated record is also stored straight into targets[k].dst for the targets
+ * whose [lo, hi) holds i -- one kernel, the peer stores issued by the threads
+ * that computed the records (no separate copy or collective).  q_out may equal
+ * q_in.  The kernel ends with a system-scope fence: once it has completed
+ * (e.g. ordered before a collective on the same stream), the stores are
+ * visible to the peers.  The CALLER orders the pushes against the peers'
+ * readers (the MD driver double-buffers the replicas).
+ * 0 <= n_targets <= LJ_MAX_PUSH_TARGETS; targets is a host array; every dst
+ * 32-byte aligned.  Asynchronous. */
+lj_status lj_integrate_push(const double *q_in, double *q_out, const double *p, const double *q_ref,
+                            int64_t begin, int64_t end, double dt, double *max_disp,
+                            const lj_push_target *targets, int n_targets, void *stream);
+
+/* CUDA IPC for the push targets (one process per GPU).  lj_ipc_get_handle:
+ * a 64-byte handle of the device allocation holding ptr, and ptr's byte offset
+ * inside it.  lj_ipc_open (another process): map that allocation (peer access
+ * enabled lazily) and return the pointer at `offset`; lj_ipc_close unmaps it
+ * (pass the pointer lj_ipc_open returned).  Synchronous. */
+lj_status lj_ipc_get_handle(const void *ptr, void *handle /* 64 bytes */, int64_t *offset);
+lj_status lj_ipc_open(const void *handle, int64_t offset, void **ptr);
+lj_status lj_ipc_close(void *ptr);
+
 /* Wrap q into [0,L) (x -= L floor(x/L); x -= L if x >= L) for atoms [0,n) and,
  * if q_ref != NULL, copy the wrapped records to q_ref (the bookkeeping
  * reference of PAPER.md:190-192). */

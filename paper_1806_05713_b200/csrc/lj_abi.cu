@@ -427,6 +427,79 @@ lj_status lj_integrate_displacement(double* q, const double* p, const double* q_
     return LJ_OK;
 }
 
+lj_status lj_integrate_push(const double* q_in, double* q_out, const double* p, const double* q_ref, int64_t begin,
+                            int64_t end, double dt, double* max_disp, const lj_push_target* targets, int n_targets,
+                            void* stream) {
+    if (begin < 0 || end < begin || end > (int64_t)INT32_MAX)
+        return fail(LJ_ERR_ARG, "integrate_push: bad range [%lld,%lld)", (long long)begin, (long long)end);
+    if (n_targets < 0 || n_targets > LJ_MAX_PUSH_TARGETS || (n_targets > 0 && !targets))
+        return fail(LJ_ERR_ARG, "integrate_push: need 0 <= n_targets <= %d and a target array", LJ_MAX_PUSH_TARGETS);
+    if (!max_disp || (end > begin && (!q_in || !q_out || !p || !q_ref)))
+        return fail(LJ_ERR_ARG, "integrate_push: null pointer");
+    if (!aligned32(q_in) || !aligned32(q_out) || !aligned32(p) || !aligned32(q_ref))
+        return fail(LJ_ERR_ARG, "integrate_push: not 32-byte aligned");
+    for (int k = 0; k < n_targets; k++) {
+        if (!targets[k].dst || !aligned32(targets[k].dst))
+            return fail(LJ_ERR_ARG, "integrate_push: target %d: null or misaligned dst", k);
+        if (targets[k].lo < 0 || targets[k].hi < targets[k].lo)
+            return fail(LJ_ERR_ARG, "integrate_push: target %d: bad rows [%lld,%lld)", k, (long long)targets[k].lo,
+                        (long long)targets[k].hi);
+    }
+    if (!std::isfinite(dt)) return fail(LJ_ERR_ARG, "integrate_push: dt not finite");
+    LJ_CUDA(launch_integrate_push(q_in, q_out, p, q_ref, begin, end, dt, max_disp, targets, n_targets,
+                                  (cudaStream_t)stream),
+            "lj_integrate_push");
+    return LJ_OK;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (liblj.so does not
+// link libcuda, so that it loads on machines without a driver).
+typedef int (*pfn_get_range)(unsigned long long*, size_t*, unsigned long long);
+
+lj_status lj_ipc_get_handle(const void* ptr, void* handle, int64_t* offset) {
+    if (!ptr || !handle || !offset) return fail(LJ_ERR_ARG, "ipc_get_handle: null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+        return fail(LJ_ERR_CUDA, "ipc_get_handle: cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (((pfn_get_range)fn)(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0)
+        return fail(LJ_ERR_ARG, "ipc_get_handle: not a device allocation");
+    cudaIpcMemHandle_t h;
+    LJ_CUDA(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base), "cudaIpcGetMemHandle");
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+    return LJ_OK;
+}
+
+lj_status lj_ipc_open(const void* handle, int64_t offset, void** ptr) {
+    if (!handle || !ptr || offset < 0) return fail(LJ_ERR_ARG, "ipc_open: bad argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    LJ_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    *ptr = (char*)base + offset;
+    return LJ_OK;
+}
+
+lj_status lj_ipc_close(void* ptr) {
+    if (!ptr) return fail(LJ_ERR_ARG, "ipc_close: null pointer");
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+        return fail(LJ_ERR_CUDA, "ipc_close: cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (((pfn_get_range)fn)(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0)
+        return fail(LJ_ERR_ARG, "ipc_close: not a mapped allocation");
+    LJ_CUDA(cudaIpcCloseMemHandle((void*)(uintptr_t)base), "cudaIpcCloseMemHandle");
+    return LJ_OK;
+}
+
 lj_status lj_wrap(double* q, double* q_ref, int64_t n, double L, void* stream) {
     LJ_TRY(check_n(n));
     if (!(L > 0.0) || !std::isfinite(L)) return fail(LJ_ERR_ARG, "wrap: L must be > 0");

@@ -91,6 +91,9 @@ cudaError_t launch_unpack(const double* in, double* xyz, int64_t n, cudaStream_t
 cudaError_t launch_integrate(double* q, const double* p, int64_t begin, int64_t end, double dt, cudaStream_t s);
 cudaError_t launch_integrate_disp(double* q, const double* p, const double* q_ref, int64_t begin, int64_t end,
                                   double dt, double* out, cudaStream_t s);
+cudaError_t launch_integrate_push(const double* q_in, double* q_out, const double* p, const double* q_ref,
+                                  int64_t begin, int64_t end, double dt, double* out, const lj_push_target* t,
+                                  int n_targets, cudaStream_t s);
 cudaError_t launch_wrap(double* q, double* q_ref, int64_t n, double L, cudaStream_t s);
 cudaError_t launch_max_disp(const double* q, const double* q_ref, int64_t begin, int64_t end, double* out,
                             cudaStream_t s);

@@ -130,6 +130,39 @@ __global__ void k_integrate_disp(rec4* __restrict__ q, const rec4* __restrict__ 
     if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// k_integrate_disp with the position exchange fused in:
+// the thread that computes q_out_i also stores it into every push target whose
+// row range holds i (a q replica of another rank, peer-mapped over NVLink), so
+// the transfer is spread over the whole drift instead of following it.  The
+// targets ride in the kernel's parameter space (__grid_constant__).
+struct PushTargets {
+    int n;
+    lj_push_target t[LJ_MAX_PUSH_TARGETS];
+};
+
+__global__ void k_integrate_push(const rec4* q_in, rec4* q_out, const rec4* __restrict__ p,   // q_in may be q_out
+                                 const rec4* __restrict__ q_ref, int64_t begin, int64_t end, double dt,
+                                 unsigned long long* out, const __grid_constant__ PushTargets T) {
+    double m = 0.0;
+    for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        rec4 a = q_in[i];
+        const rec4 b = p[i];
+        a.x = __dadd_rn(a.x, __dmul_rn(b.x, dt));
+        a.y = __dadd_rn(a.y, __dmul_rn(b.y, dt));
+        a.z = __dadd_rn(a.z, __dmul_rn(b.z, dt));
+        q_out[i] = a;
+        for (int k = 0; k < T.n; k++)
+            if (i >= T.t[k].lo && i < T.t[k].hi) reinterpret_cast<rec4*>(T.t[k].dst)[i] = a;
+        const rec4 r = q_ref[i];
+        double dx = __dsub_rn(a.x, r.x), dy = __dsub_rn(a.y, r.y), dz = __dsub_rn(a.z, r.z);
+        m = fmax(m, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz))));
+    }
+    __threadfence_system();   // the peer stores are visible system-wide once the kernel has completed
+    m = block_max(m);
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
 // KE over own rows and shifted PE over list entries inside r_c (thread per row).
 __global__ void k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p, int64_t row_begin, int64_t rows,
                          const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr,
@@ -317,6 +350,21 @@ cudaError_t launch_integrate_disp(double* q, const double* p, const double* q_re
     if (e != cudaSuccess || end <= begin) return e;
     k_integrate_disp<<<grid_for(end - begin, kThreads, 148 * 8), kThreads, 0, s>>>(
         (rec4*)q, (const rec4*)p, (const rec4*)q_ref, begin, end, dt, (unsigned long long*)out);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_integrate_push(const double* q_in, double* q_out, const double* p, const double* q_ref,
+                                  int64_t begin, int64_t end, double dt, double* out, const lj_push_target* t,
+                                  int n_targets, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+    if (e != cudaSuccess || end <= begin) return e;
+    PushTargets T;
+    T.n = n_targets;
+    for (int k = 0; k < n_targets; k++) T.t[k] = t[k];
+    k_integrate_push<<<grid_for(end - begin, kThreads, 148 * 8), kThreads, 0, s>>>(
+        (const rec4*)q_in, (rec4*)q_out, (const rec4*)p, (const rec4*)q_ref, begin, end, dt,
+        (unsigned long long*)out, T);
     g_launches++;
     return cudaGetLastError();
 }

@@ -27,6 +27,7 @@ EXPORTS = (
     "lj_cell_order",
     "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_force_step_variant", "lj_gather_probe",
     "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
+    "lj_integrate_push", "lj_ipc_get_handle", "lj_ipc_open", "lj_ipc_close",
     "lj_wrap",
     "lj_max_displacement", "lj_energy", "lj_status_string", "lj_last_error", "lj_launch_count",
     "lj_version",
@@ -45,6 +46,14 @@ _STATUS = {0: "LJ_OK", 1: "LJ_ERR_ARG", 2: "LJ_ERR_CAPACITY", 3: "LJ_ERR_CUDA", 
 class Geom(ctypes.Structure):
     """lj_geom: L (0 = open), rc (cutoff), rs (search length)."""
     _fields_ = [("L", ctypes.c_double), ("rc", ctypes.c_double), ("rs", ctypes.c_double)]
+
+
+class PushTarget(ctypes.Structure):
+    """lj_push_target: rows [lo, hi) also stored to dst (a peer's q replica)."""
+    _fields_ = [("dst", ctypes.c_void_p), ("lo", ctypes.c_int64), ("hi", ctypes.c_int64)]
+
+
+LJ_MAX_PUSH_TARGETS = 63   # include/liblj.h
 
 
 _lib = None
@@ -79,6 +88,10 @@ def load() -> ctypes.CDLL:
         "lj_list_partner_ranges": (st, [i64, i64, vp, vp, vp, vp, i32, vp, vp]),
         "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
         "lj_integrate_displacement": (st, [vp, vp, vp, i64, i64, d, vp, vp]),
+        "lj_integrate_push": (st, [vp, vp, vp, vp, i64, i64, d, vp, ctypes.POINTER(PushTarget), i32, vp]),
+        "lj_ipc_get_handle": (st, [vp, ctypes.c_char_p, ctypes.POINTER(i64)]),
+        "lj_ipc_open": (st, [ctypes.c_char_p, i64, ctypes.POINTER(vp)]),
+        "lj_ipc_close": (st, [vp]),
         "lj_wrap": (st, [vp, vp, i64, d, vp]),
         "lj_max_displacement": (st, [vp, vp, i64, i64, vp, vp]),
         "lj_energy": (st, [vp, vp, i64, Geom, i64, i64, vp, vp, vp, i32, vp, vp]),
@@ -342,6 +355,41 @@ def integrate(q: torch.Tensor, p: torch.Tensor, dt: float, begin: int = 0, end: 
     _rec(p, "p")
     _check(load().lj_integrate(_ptr(q), _ptr(p), int(begin), q.shape[0] if end is None else int(end), float(dt),
                                _stream()))
+
+
+def integrate_push(q_in: torch.Tensor, q_out: torch.Tensor, p: torch.Tensor, q_ref: torch.Tensor, dt: float,
+                   begin: int, end: int, out: torch.Tensor, targets: list[tuple[int, int, int]]) -> None:
+    """lj_integrate_push: q_out = q_in + p dt on rows [begin, end), out = max |q_out - q_ref| there,
+    and each updated row also stored into the targets (dst device pointer, lo, hi) whose [lo, hi)
+    holds it -- the drift and the position exchange in one kernel."""
+    for t, name in ((q_in, "q_in"), (q_out, "q_out"), (p, "p"), (q_ref, "q_ref")):
+        _rec(t, name)
+    if not (out.is_cuda and out.dtype == torch.float64 and out.numel() >= 1):
+        raise TypeError("integrate_push: out must be a CUDA float64 tensor")
+    arr = (PushTarget * max(len(targets), 1))(*[PushTarget(int(d), int(lo), int(hi)) for d, lo, hi in targets])
+    _check(load().lj_integrate_push(_ptr(q_in), _ptr(q_out), _ptr(p), _ptr(q_ref), int(begin), int(end), float(dt),
+                                    _ptr(out), arr, len(targets), _stream()))
+
+
+def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, t's byte offset in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _check(load().lj_ipc_get_handle(_ptr(t), h, ctypes.byref(off)))
+    return h.raw, int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    """Map another process's allocation (lj_ipc_open); returns the device pointer at offset."""
+    if len(handle) != 64:
+        raise ValueError("ipc_open: need a 64-byte handle")
+    ptr = ctypes.c_void_p()
+    _check(load().lj_ipc_open(handle, int(offset), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(load().lj_ipc_close(ctypes.c_void_p(ptr)))
 
 
 def integrate_displacement(q: torch.Tensor, p: torch.Tensor, q_ref: torch.Tensor, dt: float, begin: int, end: int,

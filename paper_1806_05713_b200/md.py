@@ -99,6 +99,20 @@ class LibBackend:
         """integrate + max_disp in one pass (lj_integrate_displacement)."""
         lj.integrate_displacement(q, p, q_ref, dt, b, e, out)
 
+    # ---- fused drift + NVLink push (exchange="push", one process per GPU) ----
+    def shared_records(self, n):
+        """A q replica other ranks push into (a plain device allocation, exported by CUDA IPC)."""
+        return torch.empty((n, 4), dtype=torch.float64, device=self.device)
+
+    def share(self, t):
+        return lj.ipc_handle(t)
+
+    def open_shared(self, handle):
+        return lj.ipc_open(*handle)
+
+    def integrate_push(self, q_in, q_out, p, q_ref, dt, b, e, out, targets):
+        lj.integrate_push(q_in, q_out, p, q_ref, dt, b, e, out, targets)
+
     def wrap(self, q, q_ref):
         lj.wrap(q, self.g.L, q_ref)
 
@@ -137,22 +151,39 @@ class LeapfrogMD:
         # owns p; every kernel ignores and preserves pads)
         self.reorder = reorder
         self.p[:, 3] = torch.arange(self.n, dtype=torch.float64, device=self.p.device)
-        if reorder:
+        # fused drift + NVLink push (exchange="push"): every rank's
+        # integrate kernel stores its updated boundary rows straight into the other
+        # ranks' q replicas (lj_integrate_push over CUDA IPC); the replicas are
+        # double-buffered (q / q_alt) so that a push of step s never lands in the
+        # buffer a slower rank's force of step s is still reading
+        if exchange not in ("allgather", "halo", "push"):
+            raise ValueError("exchange must be 'allgather', 'halo' or 'push'")
+        self.push = (exchange == "push" and self.collective and world > 1
+                     and all(hasattr(backend, f) for f in ("integrate_push", "share", "open_shared", "shared_records")))
+        if self.push:
+            q_sh = backend.shared_records(self.n)
+            q_sh.copy_(self.q)
+            self.q = q_sh
+            self.q_alt = backend.shared_records(self.n)
+            self._qbufs = [self.q, self.q_alt]
+            self._cur = 0
+            self._peers = self._open_peers()
+        elif reorder:
             self.q_alt = backend.empty_records(self.n)
+        if reorder:
             self.p_alt = backend.empty_records(self.n)
         # comm/compute overlap: the all-gather of the positions
         # runs asynchronously while the next force step computes the interior rows
         # (all partners own); boundary rows wait for it.  Needs equal slabs.
-        can = self.collective and self.n % world == 0 and hasattr(backend, "force_rows")
+        can = self.collective and self.n % world == 0 and hasattr(backend, "force_rows") and not self.push
         self.overlap = can if overlap is None else (bool(overlap) and can)
         self._pending = None                  # async all-gather of q in flight
         self.interior_rows = (self.rb, self.re)
         # halo exchange: between rebuilds each rank receives only the
         # position rows its list reads from other ranks (lj_list_partner_ranges) instead of
         # all of them; rebuilds, kdk_step and gather_all_positions() use the full all-gather
-        if exchange not in ("allgather", "halo"):
-            raise ValueError("exchange must be 'allgather' or 'halo'")
-        self.halo = exchange == "halo" and self.collective and world > 1 and hasattr(backend, "partner_ranges")
+        self.halo = (exchange in ("halo", "push") and self.collective and world > 1
+                     and hasattr(backend, "partner_ranges"))
         self._halo_plan = None                # (sends [(rank, lo, hi)], recvs [(rank, lo, hi)])
         self._stale = False                   # other ranks' rows outside the halo are out of date
         self._rebuild()
@@ -276,17 +307,32 @@ class LeapfrogMD:
                 self._allgather(self.p)          # momenta of all rows, to follow the permutation
             if hasattr(self.be, "rebuild"):      # one fused library call (lj_rebuild)
                 self.lst = self.be.rebuild(self.q, self.p, self.q_alt, self.p_alt, self.q_ref)
-                self.q, self.q_alt = self.q_alt, self.q
+                self._swap_q()
                 self.p, self.p_alt = self.p_alt, self.p
                 return
             self.be.wrap(self.q, None)
             perm = self.be.cell_order(self.q)
             self.be.permute(self.q, perm, self.q_alt)
             self.be.permute(self.p, perm, self.p_alt)
-            self.q, self.q_alt = self.q_alt, self.q
+            self._swap_q()
             self.p, self.p_alt = self.p_alt, self.p
         self.be.wrap(self.q, self.q_ref)
         self.lst = self.be.build(self.q)
+
+    def _swap_q(self):
+        """q <-> q_alt (the push mode tracks which of the two shared buffers is current:
+        every rank swaps at the same steps, so the index is the same on all ranks)."""
+        self.q, self.q_alt = self.q_alt, self.q
+        if self.push:
+            self._cur ^= 1
+
+    def _open_peers(self):
+        """Map every other rank's two q buffers: peers[b][a] = rank a's buffer b (None for self)."""
+        mine = [self.be.share(t) for t in self._qbufs]
+        table = [None] * self.world
+        dist.all_gather_object(table, mine, group=self.comm)
+        return [[None if a == self.rank else self.be.open_shared(table[a][b]) for a in range(self.world)]
+                for b in range(2)]
 
     def atom_ids(self):
         """Original atom id of every storage slot (int64, device)."""
@@ -321,7 +367,17 @@ class LeapfrogMD:
         """q += p dt on own rows, the bookkeeping check (displacement all-reduce
         MAX first), then the position exchange: a blocking all-gather + rebuild
         when the list expires, else the all-gather (asynchronous with overlap)."""
-        if hasattr(self.be, "integrate_disp"):
+        if self.push:
+            # the drift writes the other buffer and pushes the rows each peer's list
+            # reads into that peer's other buffer; the displacement all-reduce below
+            # orders every rank's pushes before any rank's next force step
+            nxt = self._cur ^ 1
+            targets = [(self._peers[nxt][a], lo, hi) for a, lo, hi in self._halo_plan[0]]
+            self.be.integrate_push(self.q, self._qbufs[nxt], self.p, self.q_ref, self.dt, self.rb, self.re,
+                                   self.disp, targets)
+            self._swap_q()
+            self._stale = True
+        elif hasattr(self.be, "integrate_disp"):
             self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, self.rb, self.re, self.disp)
         else:
             self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
@@ -331,6 +387,8 @@ class LeapfrogMD:
             self._allgather_q()
             self._rebuild()
             self.stats.rebuilds += 1
+        elif self.push:
+            pass                                   # the positions have already been pushed
         elif self.halo:
             self._halo_exchange(async_op=self.overlap)
         elif self.overlap:

@@ -115,6 +115,21 @@ def test_validation_of_the_step_entry_points(L):
     assert st == lj.LJ_ERR_ARG and b"aligned" in L.lj_last_error()
     assert L.lj_integrate_displacement(a, b, c, 0, 10, float("inf"), d, None) == lj.LJ_ERR_ARG
     assert L.lj_integrate_displacement(a, b, c, 10, 0, 0.01, d, None) == lj.LJ_ERR_ARG
+    # fused drift + push: target count, target rows / alignment, null max_disp
+    T = (lj.PushTarget * 2)(lj.PushTarget(512, 0, 10), lj.PushTarget(264, 0, 10))
+    assert L.lj_integrate_push(a, b, c, d, 0, 10, 0.01, a, T, 64, None) == lj.LJ_ERR_ARG
+    assert L.lj_integrate_push(a, b, c, d, 0, 10, 0.01, a, None, 1, None) == lj.LJ_ERR_ARG
+    st = L.lj_integrate_push(a, b, c, d, 0, 10, 0.01, a, T, 2, None)
+    assert st == lj.LJ_ERR_ARG and b"target 1" in L.lj_last_error()
+    T[1] = lj.PushTarget(768, 5, 4)
+    st = L.lj_integrate_push(a, b, c, d, 0, 10, 0.01, a, T, 2, None)
+    assert st == lj.LJ_ERR_ARG and b"bad rows" in L.lj_last_error()
+    assert L.lj_integrate_push(a, b, c, d, 0, 10, 0.01, None, T, 1, None) == lj.LJ_ERR_ARG
+    # IPC: argument checks only (a real handle needs a device)
+    assert L.lj_ipc_get_handle(None, ctypes.create_string_buffer(64), ctypes.byref(ne)) == lj.LJ_ERR_ARG
+    assert L.lj_ipc_open(None, 0, ctypes.byref(ctypes.c_void_p())) == lj.LJ_ERR_ARG
+    assert L.lj_ipc_open(b"\0" * 64, -1, ctypes.byref(ctypes.c_void_p())) == lj.LJ_ERR_ARG
+    assert L.lj_ipc_close(None) == lj.LJ_ERR_ARG
     # nothing above reached the device
     assert L.lj_launch_count() == 0
 

@@ -22,8 +22,9 @@ from paper_1806_05713_b200 import lj, md
 class OracleBackend:
     """CPU backend over the oracle with the LibBackend interface (tests only)."""
 
-    def __init__(self, n, g, row_begin, row_end, half=False):
+    def __init__(self, n, g, row_begin, row_end, half=False, shm_dir=None):
         self.n, self.g, self.rb, self.re, self.half = n, g, row_begin, row_end, half
+        self.shm_dir, self._paths = shm_dir, {}
 
     def records(self, xyz):
         out = torch.zeros((xyz.shape[0], 4), dtype=torch.float64)
@@ -91,6 +92,30 @@ class OracleBackend:
         if q_ref is not None:
             q_ref.copy_(q)
 
+    # exchange="push": the peers' q replicas are file-backed shared tensors (the CPU
+    # stand-in for CUDA IPC mappings); integrate_push stores into them directly
+    def shared_records(self, n):
+        path = os.path.join(self.shm_dir, f"q_{os.getpid()}_{len(self._paths)}.bin")
+        t = torch.from_file(path, shared=True, size=n * 4, dtype=torch.float64).view(n, 4)
+        t.zero_()
+        self._paths[t.data_ptr()] = path
+        return t
+
+    def share(self, t):
+        return self._paths[t.data_ptr()], t.shape[0]
+
+    def open_shared(self, handle):
+        path, n = handle
+        return torch.from_file(path, shared=True, size=n * 4, dtype=torch.float64).view(n, 4)
+
+    def integrate_push(self, q_in, q_out, p, q_ref, dt, b, e, out, targets):
+        new = oracle.integrate(self._xyz(q_in), self._xyz(p), dt, b, e)
+        q_out[b:e, :3] = torch.as_tensor(new[b:e])
+        q_out[b:e, 3] = q_in[b:e, 3]
+        out[0] = oracle.max_displacement(self._xyz(q_out), self._xyz(q_ref), b, e)
+        for peer, lo, hi in targets:
+            peer[lo:hi] = q_out[lo:hi]
+
     def energy(self, q, p, lst, out):
         ke, pe = oracle.energy(self._xyz(q), self._xyz(p), self.g.L, self.g.rc, lst)
         out[0], out[1] = ke, pe
@@ -104,15 +129,17 @@ def make_system(n_drop, cells=8):
     return w, q, p
 
 
-def run(rank, world, n_drop, reorder, steps, comm=None, overlap=None, exchange="allgather"):
+def run(rank, world, n_drop, reorder, steps, comm=None, overlap=None, exchange="allgather", shm_dir=None):
     # overlap needs slabs wider than 2 r_s to have interior rows: 12^3 FCC cells (L = 19)
-    w, q, p = make_system(n_drop, 12 if (overlap or exchange == "halo") else 8)
+    w, q, p = make_system(n_drop, 12 if (overlap or exchange != "allgather") else 8)
     g = lj.geom(w.L, w.rc, w.rs)
     rb, re_ = md.row_range(q.shape[0], rank, world)
-    sim = md.LeapfrogMD(OracleBackend(q.shape[0], g, rb, re_), q, p, g, w.dt, rank, world, comm,
+    sim = md.LeapfrogMD(OracleBackend(q.shape[0], g, rb, re_, shm_dir=shm_dir), q, p, g, w.dt, rank, world, comm,
                         count_interactions=False, reorder=reorder, overlap=overlap, exchange=exchange)
-    if world > 2 and exchange == "halo":
+    if world > 2 and exchange != "allgather":
         assert sim.halo and 0 < sim.halo_bytes() < (q.shape[0] - (re_ - rb)) * 32, "a halo, not everything"
+    if world > 1 and exchange == "push":
+        assert sim.push and not sim.overlap
     if world > 1 and overlap:
         assert sim.overlap
         a, b = sim.interior_rows
@@ -135,7 +162,7 @@ def _worker(rank, world, port, n_drop, reorder, steps, outdir, overlap=None, exc
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        q, p, rb, e = run(rank, world, n_drop, reorder, steps, dist.group.WORLD, overlap, exchange)
+        q, p, rb, e = run(rank, world, n_drop, reorder, steps, dist.group.WORLD, overlap, exchange, outdir)
         np.savez(os.path.join(outdir, f"r{rank}.npz"), q=q, p=p, rb=rb, e=np.array(e))
     finally:
         dist.destroy_process_group()
@@ -152,11 +179,16 @@ def free_port():
 @pytest.mark.parametrize("world,n_drop,reorder,overlap,exchange", [
     (2, 0, True, False, "allgather"), (2, 0, False, False, "allgather"), (2, 3, True, None, "allgather"),
     (2, 0, True, True, "allgather"), (2, 0, False, True, "allgather"),
-    (2, 0, True, False, "halo"), (3, 0, True, True, "halo"), (3, 0, False, False, "halo")])
+    (2, 0, True, False, "halo"), (3, 0, True, True, "halo"), (3, 0, False, False, "halo"),
+    (2, 0, True, None, "push"), (3, 0, True, None, "push"), (3, 0, False, None, "push"),
+    (2, 3, True, None, "push")])
 def test_ranks_equal_one_rank(tmp_path, world, n_drop, reorder, overlap, exchange):
     """overlap=True: the position exchange runs asynchronously while the interior
     rows' forces are computed; exchange="halo": only the rows
-    each rank's list reads are sent between rebuilds (NEXT-2) -- still bit-identical."""
+    each rank's list reads are sent between rebuilds (NEXT-2); exchange="push": the
+    drift stores those rows straight into the peers' double-buffered replicas
+    (NEXT-2 fused variant, shared files standing in for CUDA IPC) -- all
+    bit-identical to one rank."""
     steps = 12        # T = 1, dt = 0.01: the list is rebuilt every ~4-5 steps
     q1, p1, rb1, e1 = run(0, 1, n_drop, reorder, steps, overlap=overlap, exchange=exchange)
     assert rb1 >= 2, "the test must exercise rebuilds"
