@@ -236,20 +236,33 @@ class LeapfrogMD:
 
     # ---- halo exchange (NEXT-2) ----
     def _plan_halo(self):
-        """After a build: which own rows every other rank reads, and which rows of theirs we read."""
-        bounds = [row_range(self.n, s, self.world)[0] for s in range(self.world)] + [self.n]
+        """After a build: which own rows every other rank reads, and which rows of theirs we read.
+        Each owner slab is queried as two halves, so that a slab read from both of its sides
+        (P = 2: the periodic neighbour on the left and on the right is the same rank) gives
+        two short ranges instead of one that spans the slab."""
+        W = self.world
+        bounds = []
+        for s in range(W):
+            b, e = row_range(self.n, s, W)
+            bounds += [b, (b + e) // 2]
+        bounds.append(self.n)
         need = self.be.partner_ranges(self.lst, bounds)
-        mine = torch.zeros((self.world, 2), dtype=torch.int64, device=self.q.device)
-        for s, r in enumerate(need):
-            if s != self.rank and r is not None:
-                mine[s, 0], mine[s, 1] = r[0], r[1] + 1
-        table = torch.empty((self.world * self.world, 2), dtype=torch.int64, device=self.q.device)
-        dist.all_gather_into_tensor(table, mine, group=self.comm)
-        table = table.view(self.world, self.world, 2).tolist()   # table[a][s] = rows of s that a reads
-        sends = [(a, *table[a][self.rank]) for a in range(self.world)
-                 if a != self.rank and table[a][self.rank][1] > table[a][self.rank][0]]
-        recvs = [(s, *table[self.rank][s]) for s in range(self.world)
-                 if s != self.rank and table[self.rank][s][1] > table[self.rank][s][0]]
+        mine = torch.zeros((W, 2, 2), dtype=torch.int64, device=self.q.device)
+        for k, r in enumerate(need):
+            if k // 2 != self.rank and r is not None:
+                mine[k // 2, k % 2, 0], mine[k // 2, k % 2, 1] = r[0], r[1] + 1
+        table = torch.empty((W * W, 2, 2), dtype=torch.int64, device=self.q.device)
+        dist.all_gather_into_tensor(table.view(W * W * 2, 2), mine.view(W * 2, 2), group=self.comm)
+        table = table.view(W, W, 2, 2).tolist()   # table[a][s][h] = rows of half h of slab s that a reads
+
+        def ranges(a, s):
+            out = [(lo, hi) for lo, hi in table[a][s] if hi > lo]
+            if len(out) == 2 and out[0][1] >= out[1][0]:   # touching halves: one range
+                out = [(out[0][0], out[1][1])]
+            return out
+
+        sends = [(a, lo, hi) for a in range(W) if a != self.rank for lo, hi in ranges(a, self.rank)]
+        recvs = [(s, lo, hi) for s in range(W) if s != self.rank for lo, hi in ranges(self.rank, s)]
         self._halo_plan = (sends, recvs)
 
     def _halo_exchange(self, async_op: bool):
