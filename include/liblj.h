@@ -160,6 +160,32 @@ lj_status lj_force_step_ex(const double *q, double *p, int64_t n, lj_geom g, dou
                            const int32_t *sorted_list, int lanes_per_row, int ordered,
                            unsigned long long *n_interactions, void *stream);
 
+/* ---- half list without per-entry global atomics ------ */
+
+/* The cell structure of the last list build (lj_build_list[_ex] / lj_rebuild
+ * with this workspace, n and g): cell_start (device, ncell + 1 int64, ncell =
+ * floor(L/rs)^3) = the first position of every cell in the cell-sorted atom
+ * order; for cell-ordered storage (lj_rebuild's output, or lj_cell_order +
+ * lj_permute_rows before the build) cell c holds atoms [cell_start[c],
+ * cell_start[c+1]).  Asynchronous (one device copy). */
+lj_status lj_list_cell_starts(const void *workspace, size_t workspace_bytes, int64_t n, lj_geom g,
+                              int64_t *cell_start, void *stream);
+
+/* lj_force_step for a HALF list over all rows [0, n) (Alg. 3, PAPER.md
+ * P:247-267) without per-entry global atomics: one CTA per cell takes the rows
+ * [cell_start[c], cell_start[c+1]) and accumulates the p_j contributions of
+ * its rows -- and the rows' own sums -- in a shared-memory window over the 27
+ * neighbour cells' index ranges, then adds the window to p with one fp64 RED
+ * per component and atom.  Same result as lj_force_step(half = 1) up to
+ * summation order (C-12); any storage order is correct (partners outside the
+ * window take a global RED), cell-ordered storage is the fast case.
+ * lanes_per_row: 0 (= 8 | 2 << 8), 2 | 2 << 8, 4 | 2 << 8, 8 | 2 << 8 or 4 | 3 << 8.
+ * n_interactions as lj_force_step_ex.  Asynchronous. */
+lj_status lj_force_step_half_cells(const double *q, double *p, int64_t n, lj_geom g, double dt,
+                                   const int32_t *number_of_partners, const int64_t *pointer,
+                                   const int32_t *sorted_list, const int64_t *cell_start, int lanes_per_row,
+                                   unsigned long long *n_interactions, void *stream);
+
 /* ---- paper-variant ablations (not the hot path) ------- */
 
 /* Position/momentum layouts of the paper's variant axis (PAPER.md:117-126,

@@ -315,6 +315,50 @@ lj_status lj_force_step(const double* q, double* p, int64_t n, lj_geom g, double
                             nullptr, stream);
 }
 
+lj_status lj_list_cell_starts(const void* workspace, size_t workspace_bytes, int64_t n, lj_geom g,
+                              int64_t* cell_start, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, true));
+    if (!workspace || !cell_start) return fail(LJ_ERR_ARG, "list_cell_starts: null pointer");
+    const CellGrid cg = make_grid(g);
+    const BuildWorkspace W = build_workspace_layout(n, cg.ncell, 0);
+    if (workspace_bytes < W.off_atoms) return fail(LJ_ERR_ARG, "list_cell_starts: workspace too small");
+    LJ_CUDA(cudaMemcpyAsync(cell_start, (const char*)workspace + W.off_start, sizeof(int64_t) * (cg.ncell + 1),
+                            cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+            "lj_list_cell_starts");
+    return LJ_OK;
+}
+
+lj_status lj_force_step_half_cells(const double* q, double* p, int64_t n, lj_geom g, double dt,
+                                   const int32_t* number_of_partners, const int64_t* pointer,
+                                   const int32_t* sorted_list, const int64_t* cell_start, int lanes_per_row,
+                                   unsigned long long* n_interactions, void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, true));
+    if (!std::isfinite(dt)) return fail(LJ_ERR_ARG, "force_half_cells: dt not finite");
+    if (n > 0 && (!q || !p || !number_of_partners || !pointer || !cell_start))
+        return fail(LJ_ERR_ARG, "force_half_cells: null pointer");
+    if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "force_half_cells: q/p not 32-byte aligned");
+    if (lanes_per_row != 0 && lanes_per_row != (4 | (2 << 8)) && lanes_per_row != (8 | (2 << 8)) &&
+        lanes_per_row != (4 | (3 << 8)) && lanes_per_row != (2 | (2 << 8)))
+        return fail(LJ_ERR_ARG, "force_half_cells: lanes_per_row must be 0, 2|2<<8, 4|2<<8, 8|2<<8 or 4|3<<8");
+    ForceArgs a;
+    a.q = q;
+    a.p = p;
+    a.row_begin = 0;
+    a.rows = n;
+    a.npart = number_of_partners;
+    a.ptr = pointer;
+    a.list = sorted_list;
+    a.L = g.L;
+    a.rc2 = g.rc * g.rc;
+    a.dt = dt;
+    a.n_inter = n_interactions;
+    LJ_CUDA(launch_force_half_cells(a, cell_start, make_grid(g).nc, lanes_per_row, (cudaStream_t)stream),
+            "lj_force_step_half_cells");
+    return LJ_OK;
+}
+
 lj_status lj_force_step_variant(int layout, int rcp, const double* q, double* p, int64_t n, lj_geom g, double dt,
                                 int64_t row_begin, int64_t row_end, const int32_t* number_of_partners,
                                 const int64_t* pointer, const int32_t* sorted_list, int lanes_per_row,

@@ -23,6 +23,7 @@
 //  * minimum image: raw differences are checked with integer ops on the high
 //    words; the three image DADDs run only when some lane of the warp needs an
 //    image (warp-uniform branch), i.e. only for rows near a box face.
+#include <algorithm>
 #include <climits>
 
 #include "lj_internal.cuh"
@@ -174,6 +175,188 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
             pi.y += ay;
             pi.z += az;
             p[i] = pi;   // pad preserved (read back unchanged)
+        }
+    }
+    count_interactions(cnt, n_inter);
+}
+
+// ---- half list without per-entry global atomics -------
+// One CTA per cell of the build's cell grid; rows = the cell's index range
+// [cstart[c], cstart[c+1]) (in cell-ordered storage: exactly the cell's atoms).
+// Every partner j of these rows lies in one of the 27 neighbour cells, i.e. in
+// one of 27 index runs; the CTA accumulates the p_j contributions (and its own
+// rows' sums) in a shared-memory window indexed by (run, offset) and flushes
+// it once with one RED per component and atom -- coalesced, instead of three
+// random REDs per list entry.  A partner outside the window (storage not in
+// cell order, or a window larger than kWin) falls back to a global RED, so the
+// result does not depend on the storage order, only the speed does.
+constexpr int kWin = 1024;   // window slots (3 doubles each: 24 KB of shared memory)
+#ifndef LJ_HC_THREADS
+#define LJ_HC_THREADS 128    // CTA size: 8 CTAs (32 warps) per SM, so barrier waits overlap other CTAs
+#endif
+
+__device__ __forceinline__ int win_slot(int j, const int* rs, const int* rn, const int* roff) {
+    int r = 0;   // largest r with rs[r] <= j (rs ascending, padded with INT_MAX)
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) r = rs[r + st] <= j ? r + st : r;
+    const int off = j - rs[r];
+    return (off >= 0 && off < rn[r]) ? roff[r] + off : -1;
+}
+
+__device__ __forceinline__ void win_add(double* w, int slot, double v, double* gp) {
+    if (slot >= 0) atomicAdd(w + slot, v);   // shared memory
+    else atomicAdd(gp, v);                   // outside the window: global RED
+}
+
+__device__ __forceinline__ int axis_rank3(int v, int d, int nc) {   // as k_list_v4's axis_rank
+    if (v == 0) return d == 0 ? 0 : (d == 1 ? 1 : 2);
+    if (v == nc - 1) return d == 1 ? 0 : (d == -1 ? 1 : 2);
+    return d + 1;
+}
+
+template <int G, int U, int kHalfCellThreads>
+__global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
+    k_force_half_cells(const rec4* __restrict__ q, rec4* __restrict__ p, const int32_t* __restrict__ npart,
+                       const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
+                       const int64_t* __restrict__ cstart, int nc, int64_t ncell, PairConsts c,
+                       unsigned long long* n_inter) {
+    extern __shared__ double s_acc[];                 // [3][kWin]
+    __shared__ int s_rs[48], s_rn[32], s_roff[32];    // run start / length / slot offset (rank order)
+    __shared__ int s_m;
+    double* wx = s_acc;
+    double* wy = s_acc + kWin;
+    double* wz = s_acc + 2 * kWin;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int grp = tid / G, g = tid % G;
+    constexpr int NG = kHalfCellThreads / G;
+    unsigned cnt = 0;
+    for (int64_t cell = blockIdx.x; cell < ncell; cell += gridDim.x) {
+        const int64_t cs = cstart[cell];
+        const int ccnt = (int)(cstart[cell + 1] - cs);
+        __syncthreads();   // the previous cell's window has been flushed
+        if (w == 0) {
+            const int cz = (int)(cell % nc), cy = (int)((cell / nc) % nc), cx = (int)(cell / ((int64_t)nc * nc));
+            int st = INT_MAX, len = 0, rank = 27 + (lane - 27 < 0 ? 0 : lane - 27);
+            if (lane < 27) {
+                const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
+                int x = cx + dx, y = cy + dy, z = cz + dz;
+                x += x < 0 ? nc : (x >= nc ? -nc : 0);
+                y += y < 0 ? nc : (y >= nc ? -nc : 0);
+                z += z < 0 ? nc : (z >= nc ? -nc : 0);
+                const int64_t cc = ((int64_t)x * nc + y) * nc + z;
+                st = (int)cstart[cc];
+                // a half-list partner j > i >= cs lies at or after cs: runs before this
+                // cell (lower cell ids, in cell order) get no window slots
+                len = st >= cs ? (int)(cstart[cc + 1] - cstart[cc]) : 0;
+                rank = axis_rank3(cx, dx, nc) * 9 + axis_rank3(cy, dy, nc) * 3 + axis_rank3(cz, dz, nc);
+            }
+            s_rs[rank] = st;   // lanes 27..31 pad ranks 27..31 with INT_MAX
+            s_rn[rank] = len;
+            s_rs[32 + (lane & 15)] = INT_MAX;
+            __syncwarp();
+            const int myn = s_rn[lane];
+            int incl = myn;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            s_roff[lane] = incl - myn;
+            if (lane == 31) s_m = incl;
+        }
+        __syncthreads();
+        const int M = s_m;
+        const bool win = M <= kWin;   // (CTA-uniform)
+        if (win)
+            for (int k = tid; k < M; k += kHalfCellThreads) wx[k] = wy[k] = wz[k] = 0.0;
+        __syncthreads();
+        for (int base = 0; base < ccnt; base += NG) {
+            const bool active = base + grp < ccnt;
+            const int64_t i = cs + (active ? base + grp : 0);
+            const rec4 qi = load_rec(q, i);
+            const int32_t* __restrict__ lst = list + (active ? ptr[i] : 0);
+            const int n = active ? npart[i] : 0;
+            double ax = 0.0, ay = 0.0, az = 0.0;
+            int jn[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
+            for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
+                int j[U];
+                rec4 qj[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    j[u] = jn[u];
+                    qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int kn = k0 + U * G + u * G;
+                    jn[u] = kn < n ? __ldg(lst + kn) : -1;
+                }
+                double dx[U], dy[U], dz[U], r2[U];
+                int hmax = 0;
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    dx[u] = qj[u].x - qi.x;
+                    dy[u] = qj[u].y - qi.y;
+                    dz[u] = qj[u].z - qi.z;
+                    r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+                    hmax = max(hmax, __double2hiint(r2[u]));
+                }
+                if (__any_sync(0xffffffffu, hmax >= c.hi_L2q)) {   // rows near a box face: periodic images
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        dx[u] -= image_shift(dx[u], c.L, c.hi_halfL);
+                        dy[u] -= image_shift(dy[u], c.L, c.hi_halfL);
+                        dz[u] -= image_shift(dz[u], c.L, c.hi_halfL);
+                        r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const double dx_ = dx[u], dy_ = dy[u], dz_ = dz[u];
+                    const bool in = j[u] >= 0 && __double_as_longlong(r2[u]) < c.rc2_bits;
+                    if (in) {
+                        const double inv2 = fast_rcp(r2[u]);
+                        const double inv6 = inv2 * inv2 * inv2;
+                        const double df = fma(c.c48, inv6, -c.c24) * (inv6 * inv2);
+                        ax = fma(-df, dx_, ax);
+                        ay = fma(-df, dy_, ay);
+                        az = fma(-df, dz_, az);
+                        cnt++;
+                        const int sl = win ? win_slot(j[u], s_rs, s_rn, s_roff) : -1;
+                        win_add(wx, sl, df * dx_, &p[j[u]].x);
+                        win_add(wy, sl, df * dy_, &p[j[u]].y);
+                        win_add(wz, sl, df * dz_, &p[j[u]].z);
+                    }
+                }
+            }
+            unsigned dummy = 0;
+            group_reduce<G>(ax, ay, az, dummy);
+            if (active && g == 0) {
+                const int sl = win ? win_slot((int)i, s_rs, s_rn, s_roff) : -1;
+                win_add(wx, sl, ax, &p[i].x);
+                win_add(wy, sl, ay, &p[i].y);
+                win_add(wz, sl, az, &p[i].z);
+            }
+        }
+        __syncthreads();
+        if (win) {   // flush: one RED per component and touched atom, consecutive atoms per warp
+            for (int k = tid; k < M; k += kHalfCellThreads) {
+                const double vx = wx[k], vy = wy[k], vz = wz[k];
+                if (vx != 0.0 || vy != 0.0 || vz != 0.0) {
+                    int r = 0;   // largest r with s_roff[r] <= k and a non-empty run
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {
+                        const int rr = r + st;
+                        r = (rr < 27 && s_roff[rr] <= k) ? rr : r;
+                    }
+                    const int64_t a = (int64_t)s_rs[r] + (k - s_roff[r]);
+                    atomicAdd(&p[a].x, vx);
+                    atomicAdd(&p[a].y, vy);
+                    atomicAdd(&p[a].z, vz);
+                }
+            }
         }
     }
     count_interactions(cnt, n_inter);
@@ -451,6 +634,31 @@ cudaError_t launch_gu(const ForceArgs& a, int lanes, cudaStream_t s) {
 
 cudaError_t launch_force_full(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_gu<false>(a, lanes, s); }
 cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s) { return launch_gu<true>(a, lanes, s); }
+
+cudaError_t launch_force_half_cells(const ForceArgs& a, const int64_t* cstart, int nc, int lanes, cudaStream_t s) {
+    if (a.rows <= 0) return cudaSuccess;
+    const int64_t ncell = (int64_t)nc * nc * nc;
+    PairConsts c = make_consts(a);
+    const size_t smem = sizeof(double) * 3 * kWin;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const unsigned grid = (unsigned)std::min<int64_t>(ncell, (int64_t)sms * (1024 / LJ_HC_THREADS) * 8);
+    const rec4* q = (const rec4*)a.q;
+    rec4* p = (rec4*)a.p;
+#define LJ_HC(G, U) k_force_half_cells<G, U, LJ_HC_THREADS><<<grid, LJ_HC_THREADS, smem, s>>>( \
+        q, p, a.npart, a.ptr, a.list, cstart, nc, ncell, c, a.n_inter)
+    switch (lanes) {
+        case 4 | (2 << 8): LJ_HC(4, 2); break;
+        case 0:
+        case 8 | (2 << 8): LJ_HC(8, 2); break;
+        case 4 | (3 << 8): LJ_HC(4, 3); break;
+        case 2 | (2 << 8): LJ_HC(2, 2); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef LJ_HC
+    g_launches++;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cudaStream_t s) {
     if (a.rows <= 0) return cudaSuccess;

@@ -82,6 +82,7 @@ struct ForceArgs {
 };
 cudaError_t launch_force_full(const ForceArgs& a, int lanes, cudaStream_t s);
 cudaError_t launch_force_half(const ForceArgs& a, int lanes, cudaStream_t s);
+cudaError_t launch_force_half_cells(const ForceArgs& a, const int64_t* cstart, int nc, int lanes, cudaStream_t s);
 cudaError_t launch_force_ordered(const ForceArgs& a, cudaStream_t s);
 cudaError_t launch_force_variant(const ForceArgs& a, int64_t n, int layout, int rcp, int lanes, cudaStream_t s);
 cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cudaStream_t s);

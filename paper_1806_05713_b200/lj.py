@@ -8,6 +8,7 @@ no CPU fallback: if liblj.so is missing or no GPU is present, calls fail.
 from __future__ import annotations
 
 import ctypes
+import math
 import dataclasses
 import os
 
@@ -26,6 +27,7 @@ EXPORTS = (
     "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_rebuild",
     "lj_cell_order",
     "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_force_step_variant", "lj_gather_probe",
+    "lj_list_cell_starts", "lj_force_step_half_cells",
     "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
     "lj_integrate_push", "lj_ipc_get_handle", "lj_ipc_open", "lj_ipc_close",
     "lj_wrap",
@@ -84,6 +86,8 @@ def load() -> ctypes.CDLL:
         "lj_force_step_ex": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, i32, i32, vp, vp]),
         "lj_force_step_variant": (st, [i32, i32, vp, vp, i64, Geom, d, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_gather_probe": (st, [vp, i64, i64, i64, vp, vp, vp, i32, vp, vp]),
+        "lj_list_cell_starts": (st, [vp, sz, i64, Geom, vp, vp]),
+        "lj_force_step_half_cells": (st, [vp, vp, i64, Geom, d, vp, vp, vp, vp, i32, vp, vp]),
         "lj_list_interior": (st, [i64, i64, vp, vp, vp, vp, vp]),
         "lj_list_partner_ranges": (st, [i64, i64, vp, vp, vp, vp, i32, vp, vp]),
         "lj_integrate": (st, [vp, vp, i64, i64, d, vp]),
@@ -222,6 +226,16 @@ class ListBuilder:
             LJ_LIST_PADDED if self.padded else 0, _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
             self.sorted_list.numel(), ctypes.byref(ne), _ptr(self.workspace), self.workspace.numel(), _stream()))
 
+    def cell_starts(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """lj_list_cell_starts: the last build's cell starts (int64, ncell + 1) -- the cell
+        structure lj_force_step_half_cells works on."""
+        nc = int(math.floor(self.g.L / self.g.rs))
+        if out is None:
+            out = torch.empty(nc ** 3 + 1, dtype=torch.int64, device=self.device)
+        _check(load().lj_list_cell_starts(_ptr(self.workspace), self.workspace.numel(), self.n, self.g, _ptr(out),
+                                          _stream()))
+        return out
+
     def rebuild(self, q: torch.Tensor, p: torch.Tensor | None, q_out: torch.Tensor, p_out: torch.Tensor | None,
                 q_ref: torch.Tensor | None, perm: torch.Tensor) -> CSRList:
         """lj_rebuild: wrap q in place, permute (q, p) into cell order (q_out, p_out, q_ref = q_out,
@@ -300,6 +314,24 @@ def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRLis
         raise TypeError("n_interactions must be a CUDA int64 tensor")
     _check(load().lj_force_step_ex(_ptr(q), _ptr(p), q.shape[0], g, float(dt), int(lst.half), *_list_args(lst),
                                    int(lanes_per_row), int(ordered), _ptr(n_interactions), _stream()))
+
+
+def force_step_half_cells(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRList,
+                          cell_start: torch.Tensor, lanes_per_row: int = 0,
+                          n_interactions: torch.Tensor | None = None) -> None:
+    """Half-list force step without per-entry global atomics (lj_force_step_half_cells):
+    per-cell shared-memory windows over the 27 neighbour cells, flushed once."""
+    _rec(q, "q")
+    _rec(p, "p")
+    if not lst.half or lst.row_begin != 0 or lst.row_end != q.shape[0]:
+        raise ValueError("force_step_half_cells: needs a half list over all rows")
+    if not (cell_start.is_cuda and cell_start.dtype == torch.int64):
+        raise TypeError("cell_start must be a CUDA int64 tensor")
+    if n_interactions is not None and not (n_interactions.is_cuda and n_interactions.dtype == torch.int64):
+        raise TypeError("n_interactions must be a CUDA int64 tensor")
+    _check(load().lj_force_step_half_cells(_ptr(q), _ptr(p), q.shape[0], g, float(dt), _ptr(lst.number_of_partners),
+                                           _ptr(lst.pointer), _ptr(lst.sorted_list), _ptr(cell_start),
+                                           int(lanes_per_row), _ptr(n_interactions), _stream()))
 
 
 def force_step_variant(layout: str, rcp: str, q: torch.Tensor, p: torch.Tensor | None, n: int, g: Geom,

@@ -567,3 +567,63 @@ def test_integrate_displacement_fused(lj, dev, systems, rows):
     db = torch.full((1,), 5.0, dtype=torch.float64, device=dev)
     lj.integrate_displacement(qb, p, qref, 0.01, rb, re_, db)
     assert torch.equal(qa, qb) and float(da.item()) == float(db.item())
+
+
+# ---- half list without per-entry global atomics ----------
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+@pytest.mark.parametrize("lanes", [0, 8 | 512, 4 | 768])
+@pytest.mark.parametrize("padded", [True, False])
+def test_force_half_cells(lj, dev, systems, cfg, lanes, padded):
+    """Config 3 (cell order) is the fast path; configs 1 (lattice order) and 2
+    (shuffled) put partners outside the cell windows -- the global-RED path."""
+    w = systems[cfg]
+    p0 = np.random.default_rng(30 + cfg).normal(0, 1, (w.n, 3))
+    ref, S, _ = oracle_force(w, p0, True)
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    b = lj.ListBuilder(w.n, g, True, device=dev, padded=padded)
+    gl = b.build(q)
+    cst = b.cell_starts()
+    assert int(cst[-1].item()) == w.n and bool((cst[1:] >= cst[:-1]).all())
+    p = to_dev(p0, dev, pad=np.arange(w.n, dtype=np.float64))
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    lj.force_step_half_cells(q, p, g, w.dt, gl, cst, lanes_per_row=lanes, n_interactions=cnt)
+    e = oracle.parity_error(from_dev(p), ref, S)
+    assert e <= TOL, f"C-12 error {e}"
+    assert int(cnt.item()) == _entries_inside(w, True)
+    assert np.array_equal(p[:, 3].cpu().numpy(), np.arange(w.n, dtype=np.float64))   # pads preserved
+
+
+def test_force_half_cells_after_rebuild_and_dense_windows(lj, dev, systems):
+    """lj_rebuild output (cell order by construction) and a dense gas whose cell
+    windows exceed the shared-memory window (all partners take global REDs)."""
+    w = systems[1]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    p0 = to_dev(np.random.default_rng(3).normal(0, 1, (w.n, 3)), dev)
+    b = lj.ListBuilder(w.n, g, True, device=dev, padded=True)
+    qo, po = torch.empty_like(q), torch.empty_like(p0)
+    perm = torch.empty(w.n, dtype=torch.int64, device=dev)
+    gl = b.rebuild(q, p0, qo, po, None, perm)
+    cst = b.cell_starts()
+    qn, pn = from_dev(qo), from_dev(po)
+    ol = oracle.list_cells(qn, w.L, w.rs, True)
+    full = oracle.list_cells(qn, w.L, w.rs, False)
+    ref = oracle.force_step(qn, pn, w.L, w.rc, w.dt, ol)
+    S = oracle.abs_contrib(qn, pn, w.L, w.rc, w.dt, full)
+    lj.force_step_half_cells(qo, po, g, w.dt, gl, cst)
+    assert oracle.parity_error(from_dev(po), ref, S) <= TOL
+    # dense gas: 27 cells x ~190 atoms > the window
+    qg = lj_inputs.random_gas(5000, 9.9, 4, min_dist_hint=0.7)
+    g2 = lj.geom(9.9, 3.0, 3.3)
+    b2 = lj.ListBuilder(5000, g2, True, device=dev)
+    qd = to_dev(qg, dev)
+    gl2 = b2.build(qd)
+    pd0 = np.zeros((5000, 3))
+    ol2 = oracle.list_cells(qg, 9.9, 3.3, True)
+    ref2 = oracle.force_step(qg, pd0, 9.9, 3.0, 0.001, ol2)
+    S2 = oracle.abs_contrib(qg, pd0, 9.9, 3.0, 0.001, oracle.list_cells(qg, 9.9, 3.3, False))
+    pd = to_dev(pd0, dev)
+    lj.force_step_half_cells(qd, pd, g2, 0.001, gl2, b2.cell_starts())
+    assert oracle.parity_error(from_dev(pd), ref2, S2) <= TOL
