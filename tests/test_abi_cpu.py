@@ -130,6 +130,14 @@ def test_validation_of_the_step_entry_points(L):
     assert L.lj_ipc_open(None, 0, ctypes.byref(ctypes.c_void_p())) == lj.LJ_ERR_ARG
     assert L.lj_ipc_open(b"\0" * 64, -1, ctypes.byref(ctypes.c_void_p())) == lj.LJ_ERR_ARG
     assert L.lj_ipc_close(None) == lj.LJ_ERR_ARG
+    # NEXT-3 entry points: null workspace / cell starts, unsupported lanes, open box
+    assert L.lj_list_cell_starts(None, 0, 100, g, a, None) == lj.LJ_ERR_ARG
+    assert L.lj_list_cell_starts(a, 16, 100, g, a, None) == lj.LJ_ERR_ARG   # workspace too small
+    st = L.lj_force_step_half_cells(a, b, 10, g, 0.01, a, b, c, d, 16 | 512, None, None)
+    assert st == lj.LJ_ERR_ARG and b"lanes" in L.lj_last_error()
+    assert L.lj_force_step_half_cells(a, b, 10, g, 0.01, a, b, c, None, 0, None, None) == lj.LJ_ERR_ARG
+    assert L.lj_force_step_half_cells(a, b, 10, lj.Geom(0.0, 3.0, 3.3), 0.01, a, b, c, d, 0, None,
+                                      None) != lj.LJ_OK
     # nothing above reached the device
     assert L.lj_launch_count() == 0
 
