@@ -502,6 +502,8 @@ def main():
                            "sample steps; their force time is excluded from ms_per_force_step"}
         print(json.dumps(line), flush=True)
     if comm is not None:
+        barrier()
+        sim.close()   # unmap the peers' replicas (push exchange)
         dist.destroy_process_group()
 
 

@@ -113,6 +113,9 @@ class LibBackend:
     def integrate_push(self, q_in, q_out, p, q_ref, dt, b, e, out, targets):
         lj.integrate_push(q_in, q_out, p, q_ref, dt, b, e, out, targets)
 
+    def close_shared(self, ptr):
+        lj.ipc_close(ptr)
+
     def wrap(self, q, q_ref):
         lj.wrap(q, self.g.L, q_ref)
 
@@ -443,6 +446,18 @@ class LeapfrogMD:
         self.be.energy(self.q, self.p, self.lst, out)
         self._allreduce_sum(out)
         return float(out[0]), float(out[1])
+
+    def close(self):
+        """Unmap the peers' replicas (exchange="push"); the driver is unusable afterwards."""
+        if self.push and self._peers is not None:
+            closer = getattr(self.be, "close_shared", None)
+            if closer is not None:
+                for row in self._peers:
+                    for ptr in row:
+                        if ptr is not None:
+                            closer(ptr)
+            self._peers = None
+            self.push = False
 
     def interactions(self) -> int:
         """List entries inside r_c counted by the force kernels since the last call, summed over ranks."""
