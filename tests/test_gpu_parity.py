@@ -627,3 +627,40 @@ def test_force_half_cells_after_rebuild_and_dense_windows(lj, dev, systems):
     pd = to_dev(pd0, dev)
     lj.force_step_half_cells(qd, pd, g2, 0.001, gl2, b2.cell_starts())
     assert oracle.parity_error(from_dev(pd), ref2, S2) <= TOL
+
+
+@pytest.mark.parametrize("n", [0, 1, 2])
+def test_degenerate_systems_step(lj, dev, n):
+    """n = 0, 1, 2 through every step entry point: no partners -> momenta unchanged
+    (n = 2: one pair at r = 1.2, C-12 against the oracle)."""
+    L = 10.0
+    g = lj.geom(L, 3.0, 3.3)
+    xyz = np.array([[1.0, 1.0, 1.0], [2.2, 1.0, 1.0]])[:n]
+    q = to_dev(xyz.reshape(-1, 3), dev) if n else torch.empty((0, 4), dtype=torch.float64, device=dev)
+    p0 = np.random.default_rng(n).normal(0, 1, (n, 3))
+    p = to_dev(p0.reshape(-1, 3), dev) if n else torch.empty((0, 4), dtype=torch.float64, device=dev)
+    for half in (False, True):
+        b = lj.ListBuilder(n, g, half, device=dev, padded=True)
+        gl = b.build(q)
+        pa = p.clone()
+        lj.force_step(q, pa, g, 0.01, gl)
+        pb = p.clone()
+        if half:
+            lj.force_step_half_cells(q, pb, g, 0.01, gl, b.cell_starts())
+        else:
+            lj.force_step(q, pb, g, 0.01, gl, ordered=True)
+        if n:
+            ol = oracle.list_cells(xyz, L, 3.3, half)
+            ref = oracle.force_step(xyz, p0, L, 3.0, 0.01, ol)
+            S = oracle.abs_contrib(xyz, p0, L, 3.0, 0.01, oracle.list_cells(xyz, L, 3.3, False))
+            assert oracle.parity_error(from_dev(pa), ref, S) <= TOL
+            assert oracle.parity_error(from_dev(pb), ref, S) <= TOL
+            if n == 1:
+                assert torch.equal(pa, p)
+        else:
+            assert pa.numel() == 0 and pb.numel() == 0
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    q2 = q.clone()
+    lj.integrate_push(q, q2, p, q.clone(), 0.01, 0, n, out, [])
+    lj.integrate(q, p, 0.01, 0, n)
+    assert torch.equal(q, q2)
