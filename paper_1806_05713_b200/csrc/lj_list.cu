@@ -625,8 +625,15 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned short* tl = reinterpret_cast<unsigned short*>(smem);            // [8][kMaxCand + 64] slot lists
     unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);   // (aliased) unsorted staging only
-    float4* C = reinterpret_cast<float4*>(smem + 8 * (kMaxCand + 64) * 2);   // [kMaxCand + 1], last = sentinel
-    unsigned char* TM = reinterpret_cast<unsigned char*>(C + (kMaxCand + 32));
+    // staged candidates, structure of arrays (x, y, z, atom index) so that the two
+    // candidates a lane tests load straight into an fp32x2 register pair;
+    // slot kMaxCand is the sentinel
+    constexpr int kCS = kMaxCand + 32;
+    float* CX = reinterpret_cast<float*>(smem + 8 * (kMaxCand + 64) * 2);
+    float* CY = CX + kCS;
+    float* CZ = CY + kCS;
+    int* CJ = reinterpret_cast<int*>(CZ + kCS);
+    unsigned char* TM = reinterpret_cast<unsigned char*>(CJ + kCS);
     __shared__ int64_t s_start[27];
     __shared__ int s_off[28];
     __shared__ signed char s_dc[27][3];   // neighbour cell offset (-1, 0, 1) per axis
@@ -731,8 +738,12 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
                     f.x += sx;
                     f.y += sy;
                     f.z += sz;
-                    C[s_off[t] + k] = f;
-                    TM[s_off[t] + k] = (unsigned char)type_mask(f, hw, fw, a.rb2);
+                    const int m = s_off[t] + k;
+                    CX[m] = f.x;
+                    CY[m] = f.y;
+                    CZ[m] = f.z;
+                    CJ[m] = __float_as_int(f.w);
+                    TM[m] = (unsigned char)type_mask(f, hw, fw, a.rb2);
                 }
             }
         } else {
@@ -773,12 +784,18 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
                 f.x += s_dc[lo][0] * fw;
                 f.y += s_dc[lo][1] * fw;
                 f.z += s_dc[lo][2] * fw;
-                C[s] = f;
+                CX[s] = f.x;
+                CY[s] = f.y;
+                CZ[s] = f.z;
+                CJ[s] = __float_as_int(f.w);
                 TM[s] = (unsigned char)type_mask(f, hw, fw, a.rb2);
             }
         }
         for (int s = M + tid; s < M32; s += blockDim.x) TM[s] = 0;
-        if (tid == 0) C[kMaxCand] = make_float4(1e30f, 1e30f, 1e30f, __int_as_float(-1));   // sentinel
+        if (tid == 0) {   // sentinel
+            CX[kMaxCand] = CY[kMaxCand] = CZ[kMaxCand] = 1e30f;
+            CJ[kMaxCand] = -1;
+        }
         // rows of this cell and their half-cell types
         for (int t = tid; t < ccnt; t += blockDim.x) {
             const float4 f = a.qr_cell[cs + t];
@@ -851,12 +868,12 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
             const unsigned short* lst = tl + tau * kTL;
             const int len = s_tlen[tau];
             for (int k0 = 0; k0 < len; k0 += 64) {
-                const float4 c0 = C[lst[k0 + lane]], c1 = C[lst[k0 + 32 + lane]];
-                const int j0 = __float_as_int(c0.w), j1 = __float_as_int(c1.w);
+                const int s0 = lst[k0 + lane], s1 = lst[k0 + 32 + lane];
+                const int j0 = CJ[s0], j1 = CJ[s1];
                 // the two candidates side by side in packed fp32x2 registers (FADD2/FFMA2,
                 // row coordinate broadcast): same IEEE operations as the scalar form
-                const unsigned long long cx = pack_f32x2(c0.x, c1.x), cy = pack_f32x2(c0.y, c1.y),
-                                         cz = pack_f32x2(c0.z, c1.z);
+                const unsigned long long cx = pack_f32x2(CX[s0], CX[s1]), cy = pack_f32x2(CY[s0], CY[s1]),
+                                         cz = pack_f32x2(CZ[s0], CZ[s1]);
 #pragma unroll
                 for (int r = 0; r < kItemRows; r++) {
                     if (r >= nr) break;
