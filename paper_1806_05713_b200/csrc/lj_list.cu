@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
 // Rows come out ascending: candidates are staged in ascending atom order and a
 // row's chunks are visited in order by the one warp that owns the row.
 constexpr int kMaxRows = 256;   // atoms per cell handled by v4 (more -> overflow fallback)
-constexpr int kItemRows = 4;    // rows per work item
+constexpr int kItemRows = 8;    // rows per work item (8: one item per half-cell nearly always -- 8-9 items per cell, one per warp)
 constexpr int kMaxItems = kMaxRows / kItemRows + 8;
 
 __device__ __forceinline__ unsigned long long pack_f32x2(float lo, float hi) {
