@@ -93,6 +93,13 @@ lj_status lj_build_list(const double *q, int64_t n, lj_geom g, int half,
  * compact CSR; every consumer of a list (force, energy) reads only
  * [pointer[r], pointer[r] + number_of_partners[r]). */
 #define LJ_LIST_PADDED 1
+/* With LJ_LIST_PADDED only: do not synchronise.  n_entries must then point to
+ * 2 int64 of PINNED host memory, written in stream order: [0] = the number of
+ * valid entries, [1] = non-zero if a row exceeded the stride (the list is then
+ * invalid -- rebuild with the compact layout); [1] must be 0 on entry.  The
+ * caller reads them after a later synchronisation (the MD driver: at the next
+ * displacement readback), so a rebuild costs no host round trip. */
+#define LJ_LIST_DEFERRED 2
 #ifndef LJ_PADDED_ROW_STRIDE
 /* 196 entries = 784 B: not a multiple of the 128-B line, so the rows a warp
  * reads do not all start on the same DRAM channel / L2 slice (strides of 640 or

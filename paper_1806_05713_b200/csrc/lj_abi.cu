@@ -143,7 +143,9 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
     LJ_TRY(check_n(n));
     LJ_TRY(check_geom(g, true));
     LJ_TRY(check_rows(n, row_begin, row_end));
-    if (flags & ~LJ_LIST_PADDED) return fail(LJ_ERR_ARG, "build_list: unknown flags 0x%x", flags);
+    if (flags & ~(LJ_LIST_PADDED | LJ_LIST_DEFERRED)) return fail(LJ_ERR_ARG, "build_list: unknown flags 0x%x", flags);
+    if ((flags & LJ_LIST_DEFERRED) && !(flags & LJ_LIST_PADDED))
+        return fail(LJ_ERR_ARG, "build_list: LJ_LIST_DEFERRED needs LJ_LIST_PADDED");
     if (half && (row_begin != 0 || row_end != n))
         return fail(LJ_ERR_UNSUPPORTED, "half list must cover all rows [0,n) (SURVEY §8(e))");
     if (!n_entries || !pointer || (row_end > row_begin && !number_of_partners) || (n > 0 && !q))
@@ -176,6 +178,16 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
     LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, counts_scan, rows, (int64_t*)(ws + W.off_scan),
                                    W.scan_blocks, s),
             "lj_build_list/scan");
+    if (flags & LJ_LIST_DEFERRED) {   // status to the caller's pinned memory, no synchronisation
+        LJ_CUDA(cudaMemcpyAsync(n_entries, counts_scan + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                "lj_build_list/status");
+        if (rows > 0)
+            LJ_CUDA(cudaMemcpyAsync(n_entries + 1, list_row_overflow_flag(ws, W), sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, s),
+                    "lj_build_list/status");
+        LJ_CUDA(launch_padded_pointer(pointer, rows, s), "lj_build_list/pointer");
+        return LJ_OK;
+    }
     int64_t total = 0;
     int32_t row_overflow = 0;
     LJ_CUDA(cudaMemcpyAsync(&total, counts_scan + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblj.so")
 
 LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
-LJ_LIST_PADDED, LJ_PADDED_ROW_STRIDE = 1, 196   # include/liblj.h
+LJ_LIST_PADDED, LJ_LIST_DEFERRED, LJ_PADDED_ROW_STRIDE = 1, 2, 196   # include/liblj.h
 LAYOUTS = {"aos4": 0, "soa": 1, "aos3": 2, "aos8": 3}                    # LJ_LAYOUT_*
 RECIPROCALS = {"newton3": 0, "newton2": 1, "approx": 2, "ieee": 3}       # LJ_RCP_*
 
@@ -177,7 +177,7 @@ class CSRList:
     number_of_partners: torch.Tensor   # int32 [rows]
     pointer: torch.Tensor              # int64 [rows+1]
     sorted_list: torch.Tensor          # int32 [capacity] (first n_entries valid)
-    n_entries: int
+    n_entries: int                     # -1 while a deferred build is unresolved (ListBuilder.resolve)
     row_begin: int
     row_end: int
     half: bool
@@ -201,7 +201,8 @@ class ListBuilder:
     """Holds the build workspace and a growing list buffer for repeated rebuilds."""
 
     def __init__(self, n: int, g: Geom, half: bool, row_begin: int = 0, row_end: int | None = None,
-                 device=None, headroom: float = 1.15, initial_per_row: int = 0, padded: bool = False):
+                 device=None, headroom: float = 1.15, initial_per_row: int = 0, padded: bool = False,
+                 deferred: bool = False):
         self.n, self.g, self.half = int(n), g, bool(half)
         self.row_begin = int(row_begin)
         self.row_end = int(n if row_end is None else row_end)
@@ -218,13 +219,21 @@ class ListBuilder:
             initial_per_row = LJ_PADDED_ROW_STRIDE
         self.sorted_list = torch.empty(max(int(rows * initial_per_row), 1), dtype=torch.int32, device=self.device)
         self.rebuilds = 0
+        # LJ_LIST_DEFERRED (padded layout only): the build does not synchronise; its status
+        # lands in pinned memory and is checked by resolve() after a later synchronisation
+        self.deferred = bool(deferred) and padded
+        self.status = torch.zeros(2, dtype=torch.int64, pin_memory=True) if self.deferred else None
+        self._unresolved = None
+
+    def _flags(self):
+        return (LJ_LIST_PADDED if self.padded else 0) | (LJ_LIST_DEFERRED if self.deferred and self.padded else 0)
 
     def build(self, q: torch.Tensor) -> CSRList:
         _rec(q, "q")
         return self._build(lambda ne: load().lj_build_list_ex(
             _ptr(q), self.n, self.g, int(self.half), self.row_begin, self.row_end,
-            LJ_LIST_PADDED if self.padded else 0, _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
-            self.sorted_list.numel(), ctypes.byref(ne), _ptr(self.workspace), self.workspace.numel(), _stream()))
+            self._flags(), _ptr(self.npart), _ptr(self.pointer), _ptr(self.sorted_list),
+            self.sorted_list.numel(), ne, _ptr(self.workspace), self.workspace.numel(), _stream()))
 
     def cell_starts(self, out: torch.Tensor | None = None) -> torch.Tensor:
         """lj_list_cell_starts: the last build's cell starts (int64, ncell + 1) -- the cell
@@ -247,14 +256,39 @@ class ListBuilder:
             raise TypeError("rebuild: perm must be a CUDA int64 tensor of length n")
         return self._build(lambda ne: load().lj_rebuild(
             _ptr(q), _ptr(p), _ptr(q_out), _ptr(p_out), _ptr(q_ref), _ptr(perm), self.n, self.g, int(self.half),
-            self.row_begin, self.row_end, LJ_LIST_PADDED if self.padded else 0, _ptr(self.npart),
-            _ptr(self.pointer), _ptr(self.sorted_list), self.sorted_list.numel(), ctypes.byref(ne),
+            self.row_begin, self.row_end, self._flags(), _ptr(self.npart),
+            _ptr(self.pointer), _ptr(self.sorted_list), self.sorted_list.numel(), ne,
             _ptr(self.workspace), self.workspace.numel(), _stream()))
 
+    def resolve(self, lst: CSRList | None = None) -> None:
+        """Finish a deferred build once the stream has passed it (after any synchronisation):
+        fills lst.n_entries, or raises if a row overflowed the padded stride."""
+        if self._unresolved is None:
+            return
+        lst = self._unresolved if lst is None else lst
+        self._unresolved = None
+        if int(self.status[1]) != 0:
+            raise LJError(LJ_ERR_UNSUPPORTED, "deferred build: a row has more than %d partners "
+                          "(build with deferred=False: the builder then switches to the compact layout)"
+                          % LJ_PADDED_ROW_STRIDE)
+        lst.n_entries = int(self.status[0])
+
     def _build(self, call) -> CSRList:
+        if self.deferred and self.padded:
+            if self._unresolved is not None:   # the previous deferred status is still in flight
+                torch.cuda.current_stream().synchronize()
+                self.resolve()
+            self.status.zero_()
+            _check(call(ctypes.cast(self.status.data_ptr(), ctypes.POINTER(ctypes.c_int64))))
+            self.rebuilds += 1
+            rows = self.row_end - self.row_begin
+            lst = CSRList(self.npart[:rows], self.pointer, self.sorted_list, -1, self.row_begin, self.row_end,
+                          self.half, True)
+            self._unresolved = lst
+            return lst
         ne = ctypes.c_int64(0)
         for _ in range(3):
-            st = call(ne)
+            st = call(ctypes.byref(ne))
             if st == LJ_ERR_UNSUPPORTED and self.padded:   # a row longer than the stride: compact from now on
                 self.padded = False
                 continue

@@ -25,6 +25,7 @@ which has no fallback: it raises if liblj.so or the GPU is missing.
 from __future__ import annotations
 
 import dataclasses
+import math
 import os
 
 import torch
@@ -41,11 +42,20 @@ def row_range(n: int, rank: int, world: int) -> tuple[int, int]:
 class LibBackend:
     """liblj.so on the current CUDA device."""
 
-    def __init__(self, n, g: lj.Geom, row_begin, row_end, device, half=False):
+    def __init__(self, n, g: lj.Geom, row_begin, row_end, device, half=False, deferred=True):
         lj.load()
         self.device = torch.device(device)
         self.n, self.g = n, g
-        self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device, padded=True)
+        # deferred (no host round trip per rebuild) only where no row can come near the
+        # padded stride: expected full-list row length rho 4/3 pi rs^3 with 30 % margin
+        rows_expected = n / g.L ** 3 * 4.0 / 3.0 * math.pi * g.rs ** 3 if g.L > 0 else float("inf")
+        deferred = deferred and 1.3 * rows_expected < lj.LJ_PADDED_ROW_STRIDE
+        self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device, padded=True,
+                                      deferred=deferred)
+
+    def resolve(self, lst):
+        """Finish a deferred build (call after a synchronisation)."""
+        self.builder.resolve(lst)
 
     def records(self, xyz):
         t = xyz if isinstance(xyz, torch.Tensor) else torch.from_numpy(xyz)
@@ -354,10 +364,16 @@ class LeapfrogMD:
         """Original atom id of every storage slot (int64, device)."""
         return self.p[:, 3].to(torch.int64)
 
+    def _resolve(self):
+        if hasattr(self.be, "resolve"):
+            self.be.resolve(self.lst)
+
     def check_rebuild(self) -> bool:
         self.be.max_disp(self.q, self.q_ref, self.rb, self.re, self.disp)
         self._allreduce_max(self.disp)
-        if 2.0 * float(self.disp.item()) >= self.margin:
+        rebuild = 2.0 * float(self.disp.item()) >= self.margin
+        self._resolve()
+        if rebuild:
             self._rebuild()
             self.stats.rebuilds += 1
             return True
@@ -399,7 +415,9 @@ class LeapfrogMD:
             self.be.integrate(self.q, self.p, self.dt, self.rb, self.re)
             self.be.max_disp(self.q, self.q_ref, self.rb, self.re, self.disp)
         self._allreduce_max(self.disp)
-        if 2.0 * float(self.disp.item()) >= self.margin:
+        rebuild = 2.0 * float(self.disp.item()) >= self.margin
+        self._resolve()                            # the stream has passed the last (deferred) build
+        if rebuild:
             self._allgather_q()
             self._rebuild()
             self.stats.rebuilds += 1
@@ -466,4 +484,6 @@ class LeapfrogMD:
         c = self.counter.clone()
         self._allreduce_sum(c)
         self.counter.zero_()
-        return int(c.item())
+        v = int(c.item())
+        self._resolve()
+        return v

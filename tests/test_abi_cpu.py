@@ -138,6 +138,10 @@ def test_validation_of_the_step_entry_points(L):
     assert L.lj_force_step_half_cells(a, b, 10, g, 0.01, a, b, c, None, 0, None, None) == lj.LJ_ERR_ARG
     assert L.lj_force_step_half_cells(a, b, 10, lj.Geom(0.0, 3.0, 3.3), 0.01, a, b, c, d, 0, None,
                                       None) != lj.LJ_OK
+    # LJ_LIST_DEFERRED needs the padded layout; unknown flags
+    for fl in (lj.LJ_LIST_DEFERRED, 8):
+        st = L.lj_build_list_ex(a, 100, g, 0, 0, 100, fl, a, b, c, 1 << 20, ctypes.byref(ne), d, 1 << 30, None)
+        assert st == lj.LJ_ERR_ARG
     # nothing above reached the device
     assert L.lj_launch_count() == 0
 

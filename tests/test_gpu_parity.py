@@ -664,3 +664,37 @@ def test_degenerate_systems_step(lj, dev, n):
     lj.integrate_push(q, q2, p, q.clone(), 0.01, 0, n, out, [])
     lj.integrate(q, p, 0.01, 0, n)
     assert torch.equal(q, q2)
+
+
+def test_deferred_padded_build(lj, dev, systems):
+    """LJ_LIST_DEFERRED: the same list as the synchronous padded build, n_entries
+    resolved after a synchronisation; a row over the stride is reported by resolve()."""
+    w = systems[3]
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    ref = lj.ListBuilder(w.n, g, False, device=dev, padded=True).build(q)
+    b = lj.ListBuilder(w.n, g, False, device=dev, padded=True, deferred=True)
+    gl = b.build(q)
+    assert gl.n_entries == -1
+    torch.cuda.synchronize()
+    b.resolve()
+    assert gl.n_entries == ref.n_entries
+    assert torch.equal(gl.number_of_partners, ref.number_of_partners)
+    assert torch.equal(gl.pointer, ref.pointer)
+    n = w.n * lj.LJ_PADDED_ROW_STRIDE
+    v = torch.arange(n, device=dev) % lj.LJ_PADDED_ROW_STRIDE < gl.number_of_partners.repeat_interleave(
+        lj.LJ_PADDED_ROW_STRIDE)
+    assert torch.equal(gl.sorted_list[:n][v], ref.sorted_list[:n][v])
+    # a second deferred build before resolving: the builder synchronises and resolves the first
+    gl2 = b.build(q)
+    assert gl.n_entries == ref.n_entries
+    torch.cuda.synchronize()
+    b.resolve(gl2)
+    assert gl2.n_entries == ref.n_entries
+    # dense gas: rows longer than the stride -> resolve raises
+    qg = to_dev(lj_inputs.random_gas(5000, 9.9, 4), dev)
+    bd = lj.ListBuilder(5000, lj.geom(9.9, 3.0, 3.3), False, device=dev, padded=True, deferred=True)
+    bd.build(qg)
+    torch.cuda.synchronize()
+    with pytest.raises(lj.LJError):
+        bd.resolve()
