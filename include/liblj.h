@@ -300,6 +300,55 @@ lj_status lj_ipc_get_handle(const void *ptr, void *handle /* 64 bytes */, int64_
 lj_status lj_ipc_open(const void *handle, int64_t offset, void **ptr);
 lj_status lj_ipc_close(void *ptr);
 
+/* ---- the MD step as a CUDA graph ("capture the whole
+ * step ... a conditional node can skip the rebuild"; one rank) -------------- */
+
+/* Buffers of a single-rank leapfrog MD (BASELINE.json configs 4-5, reading O8 /
+ * C-16), all device memory owned by the caller and used by every launch. */
+typedef struct {
+    double *q, *p;            /* n AoS4 records each: the state, updated in place (p's pad is carried) */
+    double *q_alt, *p_alt;    /* n records each: scratch of the re-sorting rebuild (reorder != 0) */
+    double *q_ref;            /* n records: positions at the last build (written by every rebuild) */
+    int64_t *perm;            /* n: scratch (perm of the last re-sort) */
+    int64_t n;
+    lj_geom g;
+    double dt;
+    int32_t *number_of_partners; /* the current full list over rows [0, n), padded layout (LJ_LIST_PADDED) */
+    int64_t *pointer;
+    int32_t *sorted_list;
+    int64_t capacity;         /* >= n * LJ_PADDED_ROW_STRIDE */
+    void *workspace;          /* lj_build_list_workspace(n, g) bytes */
+    size_t workspace_bytes;
+    double *disp;             /* 1 double: scratch (max displacement) */
+    unsigned long long *n_interactions; /* NULL or a counter, as lj_force_step_ex */
+    int64_t *status;          /* 4 int64: [0] += rebuilds, [1] = 1 if a rebuilt row overflowed the stride
+                                 (the list is then invalid), [2] = entries of the last rebuild */
+    int reorder;              /* re-sort into cell order at every rebuild (as lj_rebuild) */
+    int steps;                /* steps per launch, 1..100000 (unrolled in the graph) */
+} lj_md_graph_desc;
+
+typedef struct lj_md_graph lj_md_graph;
+
+/* Instantiate one MD step as a CUDA graph: p += F(q) dt (lj_force_step, full
+ * list); q += p dt with the displacement (lj_integrate_displacement); a
+ * one-thread kernel takes the bookkeeping decision on the device (2 max|q -
+ * q_ref| >= rs - rc) and sets the condition of an IF node whose body is the
+ * rebuild -- reorder: lj_rebuild into q_alt / p_alt, then copied back into
+ * q / p; else lj_wrap(q, q_ref) + the build -- with its status to `status`.
+ * The d->steps steps are unrolled into one graph, so a launch is host-free: no
+ * readback per step or per rebuild.
+ * Bit-identical to the same calls made one by one.  The list must be current
+ * before the first launch (e.g. from lj_rebuild). */
+lj_status lj_md_graph_create(const lj_md_graph_desc *d, lj_md_graph **out);
+/* Run the graph's `steps` steps on `stream` (asynchronous; one launch). */
+lj_status lj_md_graph_launch(lj_md_graph *gr, void *stream);
+/* After a launch has completed: ms[k] = duration of step k's force kernel (CUDA
+ * events recorded around it inside the graph), k < min(n, steps). */
+lj_status lj_md_graph_force_ms(const lj_md_graph *gr, float *ms, int n);
+/* Kernels in one step without / in one rebuild (for launch accounting). */
+lj_status lj_md_graph_kernels(const lj_md_graph *gr, long long *per_step, long long *per_rebuild);
+lj_status lj_md_graph_destroy(lj_md_graph *gr);
+
 /* Wrap q into [0,L) (x -= L floor(x/L); x -= L if x >= L) for atoms [0,n) and,
  * if q_ref != NULL, copy the wrapped records to q_ref (the bookkeeping
  * reference of PAPER.md:190-192). */

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "lj_internal.cuh"
 
@@ -139,7 +140,7 @@ struct RebuildIO {
 lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
                           int flags, int32_t* number_of_partners, int64_t* pointer, int32_t* sorted_list,
                           int64_t capacity, int64_t* n_entries, void* workspace, size_t workspace_bytes,
-                          void* stream, const RebuildIO* rb) {
+                          void* stream, const RebuildIO* rb, int64_t* dev_status = nullptr) {
     LJ_TRY(check_n(n));
     LJ_TRY(check_geom(g, true));
     LJ_TRY(check_rows(n, row_begin, row_end));
@@ -178,6 +179,13 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
     LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, counts_scan, rows, (int64_t*)(ws + W.off_scan),
                                    W.scan_blocks, s),
             "lj_build_list/scan");
+    if (dev_status) {   // inside a CUDA graph (lj_md_graph): status to device memory, no synchronisation
+        LJ_CUDA(launch_build_status(counts_scan + rows, rows > 0 ? list_row_overflow_flag(ws, W) : nullptr,
+                                    dev_status, s),
+                "lj_md_graph/status");
+        LJ_CUDA(launch_padded_pointer(pointer, rows, s), "lj_md_graph/pointer");
+        return LJ_OK;
+    }
     if (flags & LJ_LIST_DEFERRED) {   // status to the caller's pinned memory, no synchronisation
         LJ_CUDA(cudaMemcpyAsync(n_entries, counts_scan + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
                 "lj_build_list/status");
@@ -553,6 +561,161 @@ lj_status lj_ipc_close(void* ptr) {
     if (((pfn_get_range)fn)(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0)
         return fail(LJ_ERR_ARG, "ipc_close: not a mapped allocation");
     LJ_CUDA(cudaIpcCloseMemHandle((void*)(uintptr_t)base), "cudaIpcCloseMemHandle");
+    return LJ_OK;
+}
+
+// ---- the MD step as a CUDA graph with a device-side rebuild decision --------
+struct lj_md_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    long long kernels_step = 0, kernels_rebuild = 0;
+    std::vector<cudaEvent_t> ev;   // per step: force begin, force end
+};
+
+lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
+    if (!d || !out) return fail(LJ_ERR_ARG, "md_graph: null pointer");
+    *out = nullptr;
+    const int64_t n = d->n;
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(d->g, true));
+    if (n < 1) return fail(LJ_ERR_ARG, "md_graph: n must be >= 1");
+    if (d->steps < 1 || d->steps > 100000) return fail(LJ_ERR_ARG, "md_graph: steps must be in [1, 100000]");
+    if (!std::isfinite(d->dt)) return fail(LJ_ERR_ARG, "md_graph: dt not finite");
+    if (!d->q || !d->p || !d->q_ref || !d->perm || !d->disp || !d->status || !d->number_of_partners || !d->pointer ||
+        !d->sorted_list || !d->workspace || (d->reorder && (!d->q_alt || !d->p_alt)))
+        return fail(LJ_ERR_ARG, "md_graph: null pointer");
+    if (!aligned32(d->q) || !aligned32(d->p) || !aligned32(d->q_ref) || !aligned32(d->q_alt) || !aligned32(d->p_alt))
+        return fail(LJ_ERR_ARG, "md_graph: records not 32-byte aligned");
+    if (d->capacity < n * (int64_t)LJ_PADDED_ROW_STRIDE)
+        return fail(LJ_ERR_CAPACITY, "md_graph: the padded list needs capacity %lld",
+                    (long long)(n * (int64_t)LJ_PADDED_ROW_STRIDE));
+    const CellGrid cg = make_grid(d->g);
+    const BuildWorkspace W = build_workspace_layout(n, cg.ncell, n);
+    if (d->workspace_bytes < W.total) return fail(LJ_ERR_ARG, "md_graph: workspace too small");
+    lj_md_graph* gr = new lj_md_graph();
+    cudaStream_t cs = nullptr;
+    auto done = [&](lj_status r) {
+        if (cs) cudaStreamDestroy(cs);
+        if (r != LJ_OK) {
+            lj_md_graph_destroy(gr);
+        } else {
+            *out = gr;
+        }
+        return r;
+    };
+#define LJ_G(x, where)                                              \
+    do {                                                            \
+        cudaError_t _e = (x);                                       \
+        if (_e != cudaSuccess) return done(cuda_status(_e, where)); \
+    } while (0)
+    LJ_G(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "md_graph/stream");
+    LJ_G(cudaGraphCreate(&gr->graph, 0), "md_graph/create");
+    ForceArgs fa;
+    fa.q = d->q;
+    fa.p = d->p;
+    fa.row_begin = 0;
+    fa.rows = n;
+    fa.npart = d->number_of_partners;
+    fa.ptr = d->pointer;
+    fa.list = d->sorted_list;
+    fa.L = d->g.L;
+    fa.rc2 = d->g.rc * d->g.rc;
+    fa.dt = d->dt;
+    fa.n_inter = d->n_interactions;
+    const int lanes = n >= 500000 ? (4 | (3 << 8)) : (8 | (2 << 8));   // lj_force_step_ex's defaults
+    const size_t rec = sizeof(double) * 4 * (size_t)n;
+    gr->ev.resize(2 * (size_t)d->steps, nullptr);
+    for (auto& ev : gr->ev) LJ_G(cudaEventCreate(&ev), "md_graph/event");
+    cudaGraphNode_t prev = nullptr;
+    for (int k = 0; k < d->steps; k++) {
+        // kick (between two event records: the force kernel's duration per step) + drift +
+        // displacement + the decision, captured straight into the graph after the previous step
+        LJ_G(cudaStreamBeginCaptureToGraph(cs, gr->graph, prev ? &prev : nullptr, nullptr, prev ? 1 : 0,
+                                           cudaStreamCaptureModeRelaxed),
+             "md_graph/capture");
+        long long l0 = g_launches;
+        cudaGraphConditionalHandle h = 0;
+        cudaError_t e = cudaEventRecordWithFlags(gr->ev[2 * k], cs, cudaEventRecordExternal);
+        if (e == cudaSuccess) e = launch_force_full(fa, lanes, cs);
+        if (e == cudaSuccess) e = cudaEventRecordWithFlags(gr->ev[2 * k + 1], cs, cudaEventRecordExternal);
+        if (e == cudaSuccess) e = launch_integrate_disp(d->q, d->p, d->q_ref, 0, n, d->dt, d->disp, cs);
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, gr->graph, 0, cudaGraphCondAssignDefault);
+        if (e == cudaSuccess) e = launch_md_decide(d->disp, d->g.rs - d->g.rc, h, d->status, cs);
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        cudaStreamCaptureStatus cst;
+        if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps);
+        std::vector<cudaGraphNode_t> leaf;
+        if (e == cudaSuccess) leaf.assign(deps, deps + ndeps);
+        cudaGraph_t tmp;
+        cudaError_t e2 = cudaStreamEndCapture(cs, &tmp);
+        LJ_G(e, "md_graph/step");
+        LJ_G(e2, "md_graph/capture-end");
+        if (k == 0) gr->kernels_step = g_launches - l0;
+        // IF (rebuild): the body is the bookkeeping rebuild, captured into the conditional's graph
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        LJ_G(cudaGraphAddNode(&prev, gr->graph, leaf.data(), leaf.size(), &cp), "md_graph/conditional");
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        LJ_G(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
+             "md_graph/capture-body");
+        l0 = g_launches;
+        lj_status st = LJ_OK;
+        if (d->reorder) {   // as lj_rebuild, then the permuted state back into q / p
+            RebuildIO io{d->q, d->p, d->q_alt, d->p_alt, d->q_ref, d->perm};
+            st = build_list_impl(d->q_alt, n, d->g, 0, 0, n, LJ_LIST_PADDED, d->number_of_partners, d->pointer,
+                                 d->sorted_list, d->capacity, d->status + 2, d->workspace, d->workspace_bytes, cs,
+                                 &io, d->status);
+            if (st == LJ_OK) e = cudaMemcpyAsync(d->q, d->q_alt, rec, cudaMemcpyDeviceToDevice, cs);
+            if (st == LJ_OK && e == cudaSuccess)
+                e = cudaMemcpyAsync(d->p, d->p_alt, rec, cudaMemcpyDeviceToDevice, cs);
+        } else {            // wrap + snapshot, then the list (as lj_wrap + lj_build_list_ex)
+            e = launch_wrap(d->q, d->q_ref, n, d->g.L, cs);
+            if (e == cudaSuccess)
+                st = build_list_impl(d->q, n, d->g, 0, 0, n, LJ_LIST_PADDED, d->number_of_partners, d->pointer,
+                                     d->sorted_list, d->capacity, d->status + 2, d->workspace, d->workspace_bytes,
+                                     cs, nullptr, d->status);
+        }
+        e2 = cudaStreamEndCapture(cs, &tmp);
+        if (st != LJ_OK) return done(st);
+        LJ_G(e, "md_graph/rebuild");
+        LJ_G(e2, "md_graph/capture-body-end");
+        if (k == 0) gr->kernels_rebuild = g_launches - l0;
+    }
+    LJ_G(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "md_graph/instantiate");
+#undef LJ_G
+    return done(LJ_OK);
+}
+
+lj_status lj_md_graph_force_ms(const lj_md_graph* gr, float* ms, int n) {
+    if (!gr || !ms || n < 0 || 2 * (size_t)n > gr->ev.size()) return fail(LJ_ERR_ARG, "md_graph_force_ms: bad argument");
+    for (int k = 0; k < n; k++) LJ_CUDA(cudaEventElapsedTime(ms + k, gr->ev[2 * k], gr->ev[2 * k + 1]), "event");
+    return LJ_OK;
+}
+
+lj_status lj_md_graph_launch(lj_md_graph* gr, void* stream) {
+    if (!gr || !gr->exec) return fail(LJ_ERR_ARG, "md_graph_launch: bad argument");
+    LJ_CUDA(cudaGraphLaunch(gr->exec, (cudaStream_t)stream), "cudaGraphLaunch");
+    return LJ_OK;
+}
+
+lj_status lj_md_graph_kernels(const lj_md_graph* gr, long long* per_step, long long* per_rebuild) {
+    if (!gr || !per_step || !per_rebuild) return fail(LJ_ERR_ARG, "md_graph_kernels: null pointer");
+    *per_step = gr->kernels_step;
+    *per_rebuild = gr->kernels_rebuild;
+    return LJ_OK;
+}
+
+lj_status lj_md_graph_destroy(lj_md_graph* gr) {
+    if (!gr) return LJ_OK;
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    if (gr->graph) cudaGraphDestroy(gr->graph);
+    for (auto ev : gr->ev)
+        if (ev) cudaEventDestroy(ev);
+    delete gr;
     return LJ_OK;
 }
 

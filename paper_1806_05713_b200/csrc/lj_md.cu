@@ -163,6 +163,25 @@ __global__ void k_integrate_push(const rec4* q_in, rec4* q_out, const rec4* __re
     if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// ---- device-side step control (CUDA graph with a conditional rebuild) ------
+// The bookkeeping decision of the MD step (reading C-16: rebuild when
+// 2 max|q - q_ref| >= r_s - r_c) taken on the device: sets the graph's IF
+// condition and counts rebuilds in status[0].
+__global__ void k_md_decide(const double* __restrict__ disp, double margin, cudaGraphConditionalHandle h,
+                            int64_t* status) {
+    const bool r = 2.0 * disp[0] >= margin;
+    cudaGraphSetConditional(h, r ? 1u : 0u);
+    if (r) status[0] += 1;
+}
+
+// A build inside a graph: its entry count to status[2], a row over the padded
+// stride to status[1] (sticky).
+__global__ void k_build_status(const int64_t* __restrict__ total, const int32_t* __restrict__ row_overflow,
+                               int64_t* status) {
+    status[2] = *total;
+    if (row_overflow && *row_overflow) status[1] = 1;
+}
+
 // KE over own rows and shifted PE over list entries inside r_c (thread per row).
 __global__ void k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p, int64_t row_begin, int64_t rows,
                          const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr,
@@ -365,6 +384,19 @@ cudaError_t launch_integrate_push(const double* q_in, double* q_out, const doubl
     k_integrate_push<<<grid_for(end - begin, kThreads, 148 * 8), kThreads, 0, s>>>(
         (const rec4*)q_in, (rec4*)q_out, (const rec4*)p, (const rec4*)q_ref, begin, end, dt,
         (unsigned long long*)out, T);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_md_decide(const double* disp, double margin, cudaGraphConditionalHandle h, int64_t* status,
+                             cudaStream_t s) {
+    k_md_decide<<<1, 1, 0, s>>>(disp, margin, h, status);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_status(const int64_t* total, const int32_t* row_overflow, int64_t* status, cudaStream_t s) {
+    k_build_status<<<1, 1, 0, s>>>(total, row_overflow, status);
     g_launches++;
     return cudaGetLastError();
 }

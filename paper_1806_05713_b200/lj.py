@@ -28,6 +28,7 @@ EXPORTS = (
     "lj_cell_order",
     "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_force_step_variant", "lj_gather_probe",
     "lj_list_cell_starts", "lj_force_step_half_cells",
+    "lj_md_graph_create", "lj_md_graph_launch", "lj_md_graph_force_ms", "lj_md_graph_kernels", "lj_md_graph_destroy",
     "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
     "lj_integrate_push", "lj_ipc_get_handle", "lj_ipc_open", "lj_ipc_close",
     "lj_wrap",
@@ -56,6 +57,16 @@ class PushTarget(ctypes.Structure):
 
 
 LJ_MAX_PUSH_TARGETS = 63   # include/liblj.h
+
+
+class MDGraphDesc(ctypes.Structure):
+    """lj_md_graph_desc (include/liblj.h)."""
+    _fields_ = [("q", ctypes.c_void_p), ("p", ctypes.c_void_p), ("q_alt", ctypes.c_void_p), ("p_alt", ctypes.c_void_p),
+                ("q_ref", ctypes.c_void_p), ("perm", ctypes.c_void_p), ("n", ctypes.c_int64), ("g", Geom),
+                ("dt", ctypes.c_double), ("number_of_partners", ctypes.c_void_p), ("pointer", ctypes.c_void_p),
+                ("sorted_list", ctypes.c_void_p), ("capacity", ctypes.c_int64), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t), ("disp", ctypes.c_void_p), ("n_interactions", ctypes.c_void_p),
+                ("status", ctypes.c_void_p), ("reorder", ctypes.c_int), ("steps", ctypes.c_int)]
 
 
 _lib = None
@@ -87,6 +98,11 @@ def load() -> ctypes.CDLL:
         "lj_force_step_variant": (st, [i32, i32, vp, vp, i64, Geom, d, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_gather_probe": (st, [vp, i64, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_list_cell_starts": (st, [vp, sz, i64, Geom, vp, vp]),
+        "lj_md_graph_create": (st, [ctypes.POINTER(MDGraphDesc), ctypes.POINTER(vp)]),
+        "lj_md_graph_launch": (st, [vp, vp]),
+        "lj_md_graph_force_ms": (st, [vp, ctypes.POINTER(ctypes.c_float), i32]),
+        "lj_md_graph_kernels": (st, [vp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
+        "lj_md_graph_destroy": (st, [vp]),
         "lj_force_step_half_cells": (st, [vp, vp, i64, Geom, d, vp, vp, vp, vp, i32, vp, vp]),
         "lj_list_interior": (st, [i64, i64, vp, vp, vp, vp, vp]),
         "lj_list_partner_ranges": (st, [i64, i64, vp, vp, vp, vp, i32, vp, vp]),
@@ -348,6 +364,54 @@ def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRLis
         raise TypeError("n_interactions must be a CUDA int64 tensor")
     _check(load().lj_force_step_ex(_ptr(q), _ptr(p), q.shape[0], g, float(dt), int(lst.half), *_list_args(lst),
                                    int(lanes_per_row), int(ordered), _ptr(n_interactions), _stream()))
+
+
+class MDGraph:
+    """lj_md_graph: `steps` leapfrog steps (kick, drift + displacement, device-side rebuild
+    decision, conditional rebuild) as one CUDA graph.  Holds references to every buffer."""
+
+    def __init__(self, q, p, q_alt, p_alt, q_ref, perm, g: Geom, dt: float, builder: "ListBuilder",
+                 disp, counter, status, reorder: bool, steps: int):
+        for t, name in ((q, "q"), (p, "p"), (q_ref, "q_ref")):
+            _rec(t, name)
+        if not builder.padded:
+            raise ValueError("MDGraph: needs the padded list layout")
+        self._keep = (q, p, q_alt, p_alt, q_ref, perm, builder, disp, counter, status)
+        self.steps = int(steps)
+        d = MDGraphDesc(_ptr(q).value, _ptr(p).value, _ptr(q_alt).value if q_alt is not None else None,
+                        _ptr(p_alt).value if p_alt is not None else None, _ptr(q_ref).value, _ptr(perm).value,
+                        q.shape[0], g, float(dt), _ptr(builder.npart).value, _ptr(builder.pointer).value,
+                        _ptr(builder.sorted_list).value, builder.sorted_list.numel(), _ptr(builder.workspace).value,
+                        builder.workspace.numel(), _ptr(disp).value, _ptr(counter).value if counter is not None
+                        else None, _ptr(status).value, int(bool(reorder)), self.steps)
+        h = ctypes.c_void_p()
+        _check(load().lj_md_graph_create(ctypes.byref(d), ctypes.byref(h)))
+        self._h = h
+
+    def launch(self):
+        _check(load().lj_md_graph_launch(self._h, _stream()))
+
+    def force_ms(self) -> list[float]:
+        """Per-step force-kernel durations of the last (completed) launch."""
+        out = (ctypes.c_float * self.steps)()
+        _check(load().lj_md_graph_force_ms(self._h, out, self.steps))
+        return list(out)
+
+    def kernels(self) -> tuple[int, int]:
+        a, b = ctypes.c_longlong(), ctypes.c_longlong()
+        _check(load().lj_md_graph_kernels(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if self._h is not None:
+            load().lj_md_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
 
 def force_step_half_cells(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRList,

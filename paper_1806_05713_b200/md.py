@@ -139,6 +139,33 @@ class StepStats:
     steps: int = 0
 
 
+class StepGraph:
+    """A LeapfrogMD.graph(): the steps run on the device without host round trips."""
+
+    def __init__(self, sim, g, status):
+        self.sim, self.g, self.status = sim, g, status
+        self._seen = 0
+
+    def launch(self):
+        self.g.launch()
+
+    def finish(self):
+        """After the launch has completed: rebuild count, list size, overflow check."""
+        st = self.status.tolist()
+        if st[1]:
+            raise lj.LJError(lj.LJ_ERR_UNSUPPORTED, "graph rebuild: a row exceeded the padded stride")
+        new = st[0] - self._seen
+        self._seen = st[0]
+        self.sim.stats.rebuilds += new
+        self.sim.stats.steps += self.g.steps
+        if new:
+            self.sim.lst.n_entries = int(st[2])
+        return new
+
+    def close(self):
+        self.g.close()
+
+
 class LeapfrogMD:
     """Row-split leapfrog MD.  `comm` is None for a single rank, else a
     torch.distributed process group (NCCL on GPUs, gloo in CPU tests)."""
@@ -464,6 +491,24 @@ class LeapfrogMD:
         self.be.energy(self.q, self.p, self.lst, out)
         self._allreduce_sum(out)
         return float(out[0]), float(out[1])
+
+    # ---- the step as a CUDA graph (NEXT-1: "capture the whole step"; one rank) ----
+    def graph(self, steps: int) -> "StepGraph":
+        """The next `steps` leapfrog steps (as step()) as one CUDA graph with a device-side
+        rebuild decision (lj_md_graph): launch with .launch(), then .finish() after a
+        synchronisation to fold the rebuilds into the driver's state."""
+        if self.collective or not hasattr(self.be, "builder"):
+            raise ValueError("graph: one rank with the liblj backend only")
+        torch.cuda.current_stream().synchronize()
+        self.sync_positions()
+        self._resolve()
+        if getattr(self.be, "perm", None) is None:
+            self.be.perm = torch.empty(self.n, dtype=torch.int64, device=self.q.device)
+        status = torch.zeros(4, dtype=torch.int64, device=self.q.device)
+        g = lj.MDGraph(self.q, self.p, self.q_alt if self.reorder else None, self.p_alt if self.reorder else None,
+                       self.q_ref, self.be.perm, self.g, self.dt, self.be.builder, self.disp, self.counter, status,
+                       self.reorder, steps)
+        return StepGraph(self, g, status)
 
     def close(self):
         """Unmap the peers' replicas (exchange="push"); the driver is unusable afterwards."""
