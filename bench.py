@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--order", default=None, choices=["lattice", "shuffled", "cell"],
                     help="storage order; default: config 2 shuffled, 3 cell, 4/5 cell (re-sorted at every rebuild)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="configs 2/3: launch every force step eagerly")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every step eagerly (configs 2/3: no force replay; MD configs: host-side step control)")
     ap.add_argument("--no-overlap", action="store_true", help="P > 1: blocking all-gather (no comm/compute overlap)")
     ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo", "push"],
                     help="P > 1: position exchange between rebuilds (halo = only the rows each rank's list reads, "
@@ -289,6 +290,12 @@ def main():
                 b.record(stream)
                 f_ev.append((a, b))
             lj_graph_launches[0] += launches_per_replay
+    # MD configs on one rank: the whole step -- kick, drift + displacement, the rebuild
+    # decision and the conditional rebuild -- as one CUDA graph over the K timed steps
+    # (lj_md_graph, device-side decision: no host round trip per step or rebuild)
+    md_graph = None
+    if not force_only and not args.no_graph and not sim.collective and every == 0:
+        md_graph = sim.graph(args.steps)
     lj_graph_launches = [0]
     sim.interactions()   # reset counter
     reb0 = sim.stats.rebuilds
@@ -299,14 +306,22 @@ def main():
     launches0 = lj.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for k in range(args.steps):
-        e = one_step(True, sample=(every > 0 and not force_only and k % every == 0))
-        if e is not None:
-            energies.append((k, e[0], e[1]))
+    if md_graph is not None:
+        md_graph.launch()
+    else:
+        for k in range(args.steps):
+            e = one_step(True, sample=(every > 0 and not force_only and k % every == 0))
+            if e is not None:
+                energies.append((k, e[0], e[1]))
     sim.sync_positions()
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    if md_graph is not None:
+        graph_rebuilds = md_graph.finish()
+        per_step, per_rebuild = md_graph.g.kernels()
+        lj_graph_launches[0] = per_step * args.steps + per_rebuild * graph_rebuilds
+        f_ms_graph = md_graph.g.force_ms()
     launches = lj.launch_count() - launches0 + lj_graph_launches[0]   # graph replays launch without the host
     ck = clocks.stop()
     ms = t0.elapsed_time(t1)
@@ -318,7 +333,7 @@ def main():
     pairs = entries_inside if half else entries_inside / 2.0
     value = pairs / (ms_max * 1e-3)
     rebuilds = sim.stats.rebuilds - reb0
-    force_ms = [a.elapsed_time(b) for a, b in f_ev]
+    force_ms = f_ms_graph if md_graph is not None else [a.elapsed_time(b) for a, b in f_ev]
     force_avg = sum(force_ms) / len(force_ms)
     entries_per_launch = sim.lst.n_entries       # own rows (last list)
 
@@ -487,7 +502,9 @@ def main():
                              % (4 * sim.lst.n_entries / 1e9, 4 * sim.lst.sorted_list.numel() / 1e9, 64 * w.n / 1e6),
                        "rebuilds_in_timed_steps": rebuilds},
             "ms_per_force_step": force_avg,
-            "cuda_graph": graph is not None,
+            "cuda_graph": (graph is not None or md_graph is not None),
+            "step_control": ("device (lj_md_graph: conditional rebuild node, one graph launch for the timed steps)"
+                             if md_graph is not None else "host"),
             "roofline": roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         }

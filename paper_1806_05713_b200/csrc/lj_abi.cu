@@ -686,6 +686,8 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
         if (k == 0) gr->kernels_rebuild = g_launches - l0;
     }
     LJ_G(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "md_graph/instantiate");
+    LJ_G(cudaGraphUpload(gr->exec, cs), "md_graph/upload");   // the first launch pays no upload
+    LJ_G(cudaStreamSynchronize(cs), "md_graph/upload");
 #undef LJ_G
     return done(LJ_OK);
 }
