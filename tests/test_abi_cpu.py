@@ -142,6 +142,21 @@ def test_validation_of_the_step_entry_points(L):
     for fl in (lj.LJ_LIST_DEFERRED, 8):
         st = L.lj_build_list_ex(a, 100, g, 0, 0, 100, fl, a, b, c, 1 << 20, ctypes.byref(ne), d, 1 << 30, None)
         assert st == lj.LJ_ERR_ARG
+    # lj_md_graph: descriptor checks before any CUDA call
+    h = ctypes.c_void_p()
+    assert L.lj_md_graph_create(None, ctypes.byref(h)) == lj.LJ_ERR_ARG
+    dsc = lj.MDGraphDesc(256, 512, 768, 1024, 1280, 1536, 100, g, 0.01, 256, 512, 768, 100 * 196, 1024, 1 << 30,
+                         256, None, 512, 1, 0)
+    st = L.lj_md_graph_create(ctypes.byref(dsc), ctypes.byref(h))
+    assert st == lj.LJ_ERR_ARG and b"steps" in L.lj_last_error()
+    dsc.steps = 5
+    dsc.capacity = 100
+    assert L.lj_md_graph_create(ctypes.byref(dsc), ctypes.byref(h)) == lj.LJ_ERR_CAPACITY
+    dsc.capacity = 100 * 196
+    dsc.q_alt = None
+    assert L.lj_md_graph_create(ctypes.byref(dsc), ctypes.byref(h)) == lj.LJ_ERR_ARG   # reorder needs q_alt
+    assert L.lj_md_graph_launch(None, None) == lj.LJ_ERR_ARG
+    assert L.lj_md_graph_destroy(None) == lj.LJ_OK
     # nothing above reached the device
     assert L.lj_launch_count() == 0
 
