@@ -1,22 +1,25 @@
 """MD driver over the C ABI: leapfrog velocity Verlet with the bookkeeping
 rebuild (readings O8, C-16), row-split across ranks
- with a per-step all-gather of positions.
+ with a per-step exchange of positions.
 
 One rank per GPU.  Rank r owns atoms/rows [r N/P, (r+1) N/P): it keeps the
 replicated positions q (N AoS4 records), its own momenta p (global-indexed,
 only own rows meaningful), its own bookkeeping reference q_ref and the CSR list
 of its own rows.  Per step (SURVEY §3 call stack 4):
 
-    force(dt) on own rows          -- liblj lj_force_step (kernel)
-    integrate(dt) on own rows      -- liblj lj_integrate (kernel)
-    disp = max |q - q_ref| own     -- liblj lj_max_displacement (kernel)
+    force(dt) on own rows          -- lj_force_step (kernel)
+    q += p dt; disp = max|q-q_ref| -- lj_integrate_displacement (one kernel)
     all-reduce MAX disp            -- torch.distributed, P > 1 only
     if 2 disp >= rs - rc:          -- host decision (one 8-byte readback)
         all-gather q; rebuild      -- lj_rebuild (wrap + cell order + list)
-    else: all-gather q             -- NCCL, P > 1 only; asynchronous with
-                                      overlap: the next force step computes the
-                                      interior rows (partners all own,
-                                      lj_list_interior) while it is in flight
+    else: exchange q               -- P > 1 only: NCCL all-gather (asynchronous
+                                      with overlap: the next force step computes
+                                      the interior rows while it is in flight),
+                                      halo send/recv, or the drift kernel's own
+                                      NVLink push (exchange="push")
+
+On one rank, LeapfrogMD.graph(K) runs K such steps as one CUDA graph with the
+rebuild decision on the device (lj_md_graph: no host round trip).
 
 The compute backend is injectable so the multi-rank plumbing can be tested on
 CPU with gloo (tests/test_dist_gloo.py); the product backend is LibBackend,
@@ -52,6 +55,7 @@ class LibBackend:
         deferred = deferred and 1.3 * rows_expected < lj.LJ_PADDED_ROW_STRIDE
         self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device, padded=True,
                                       deferred=deferred)
+        self.perm = None   # scratch of the re-sorting rebuild (allocated on first use)
 
     def resolve(self, lst):
         """Finish a deferred build (call after a synchronisation)."""
@@ -69,7 +73,7 @@ class LibBackend:
 
     def rebuild(self, q, p, q_out, p_out, q_ref):
         """Fused wrap + cell-order permutation + list build (lj_rebuild, one cell pass)."""
-        if not hasattr(self, "perm"):
+        if self.perm is None:
             self.perm = torch.empty(self.n, dtype=torch.int64, device=self.device)
         return self.builder.rebuild(q, p, q_out, p_out, q_ref, self.perm)
 
