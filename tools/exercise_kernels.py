@@ -58,6 +58,19 @@ def main():
     sim.start_leapfrog()
     for k in range(12):
         sim.step(sample=(k == 5))
+    # NEXT-3 half list with shared-memory windows, NEXT-2 fused drift + push (emulated
+    # peer), the MD step as a CUDA graph with the conditional rebuild
+    bh = lj.ListBuilder(w3.n, g, True, device=dev, padded=True)
+    lh = bh.build(q3)
+    lj.force_step_half_cells(q3, p.clone(), g, w3.dt, lh, bh.cell_starts())
+    peer = torch.zeros_like(q3)
+    lj.integrate_push(q3, q3.clone(), p, qr, w3.dt, 0, w3.n, torch.zeros(1, dtype=torch.float64, device=dev),
+                      [(peer.data_ptr(), 100, 900)])
+    gr = md.LeapfrogMD(md.LibBackend(wm.n, gm, 0, wm.n, dev), wm.q, wm.p, gm, wm.dt).graph(8)
+    gr.launch()
+    torch.cuda.synchronize()
+    gr.finish()
+    gr.close()
     torch.cuda.synchronize()
     print("sanitize run ok, launches", lj.launch_count())
 
