@@ -303,8 +303,12 @@ def main():
     # decision and the conditional rebuild -- as one CUDA graph over the K timed steps
     # (lj_md_graph, device-side decision: no host round trip per step or rebuild)
     md_graph = None
+    graph_note = ""
     if not force_only and not args.no_graph and not sim.collective and every == 0:
-        md_graph = sim.graph(args.steps)
+        try:
+            md_graph = sim.graph(args.steps)
+        except lj.LJError as ex:   # e.g. a driver without conditional graph nodes: eager GPU steps
+            graph_note = f" (graph unavailable: {ex})"
     lj_graph_launches = [0]
     sim.interactions()   # reset counter
     reb0 = sim.stats.rebuilds
@@ -519,7 +523,7 @@ def main():
             "interactions_counted": ("once (q fixed in the force-only configs), x steps" if counted_once is not None
                                      else "live, every timed step (kernel counter)"),
             "step_control": ("device (lj_md_graph: conditional rebuild node, one graph launch for the timed steps)"
-                             if md_graph is not None else "host"),
+                             if md_graph is not None else "host" + graph_note),
             "roofline": roof,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         }

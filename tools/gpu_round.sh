@@ -3,6 +3,7 @@ set -x
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?; tail -1 gpurun_out/smoke.log
 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?
+python tools/exercise_kernels.py > gpurun_out/exercise.log 2>&1; echo exercise=$?; tail -1 gpurun_out/exercise.log
 LJ_FORCE_COLLECTIVES=1 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 20 --warmup 5 --no-e2e > gpurun_out/bench_torchrun.log 2>&1; echo torchrun=$?
 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref=$?
 # ncu does not list the kernel nodes of a graph with conditional nodes: the launch list and
