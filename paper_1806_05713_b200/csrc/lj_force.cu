@@ -195,12 +195,16 @@ constexpr int kWin = 1024;   // window slots (3 doubles each: 24 KB of shared me
 #define LJ_HC_THREADS 128    // CTA size: 8 CTAs (32 warps) per SM, so barrier waits overlap other CTAs
 #endif
 
-__device__ __forceinline__ int win_slot(int j, const int* rs, const int* rn, const int* roff) {
-    int r = 0;   // largest r with rs[r] <= j (rs ascending, padded with INT_MAX)
+// Slot of partner j in the window: the window is a short ascending list of
+// contiguous index segments (adjacent neighbour runs merged: ~5 for an interior
+// cell), ss = segment starts padded with INT_MAX, fin = (segment end, slot - index).
+template <int STEPS>
+__device__ __forceinline__ int win_slot(int j, const int* ss, const int2* fin) {
+    int r = 0;   // largest r with ss[r] <= j
 #pragma unroll
-    for (int st = 16; st > 0; st >>= 1) r = rs[r + st] <= j ? r + st : r;
-    const int off = j - rs[r];
-    return (off >= 0 && off < rn[r]) ? roff[r] + off : -1;
+    for (int st = 1 << (STEPS - 1); st > 0; st >>= 1) r = ss[r + st] <= j ? r + st : r;
+    const int2 f = fin[r];
+    return (j >= ss[r] && j < f.x) ? j + f.y : -1;
 }
 
 __device__ __forceinline__ void win_add(double* w, int slot, double v, double* gp) {
@@ -221,12 +225,15 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
                        const int64_t* __restrict__ cstart, int nc, int64_t ncell, PairConsts c,
                        unsigned long long* n_inter) {
     extern __shared__ double s_acc[];                 // [3][kWin]
-    __shared__ int s_rs[48], s_rn[32], s_roff[32];    // run start / length / slot offset (rank order)
-    __shared__ int s_m;
+    __shared__ int s_rs[32], s_rn[32];                // neighbour runs in ascending cell id (rank order)
+    __shared__ int s_ss[64], s_soff[64];              // window segments: start index, first slot (INT_MAX pad)
+    __shared__ int2 s_fin[32];                        // window segments: (end index, slot - index)
+    __shared__ int s_m, s_nseg;
     double* wx = s_acc;
     double* wy = s_acc + kWin;
     double* wz = s_acc + 2 * kWin;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
     const int grp = tid / G, g = tid % G;
     constexpr int NG = kHalfCellThreads / G;
     unsigned cnt = 0;
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
         __syncthreads();   // the previous cell's window has been flushed
         if (w == 0) {
             const int cz = (int)(cell % nc), cy = (int)((cell / nc) % nc), cx = (int)(cell / ((int64_t)nc * nc));
-            int st = INT_MAX, len = 0, rank = 27 + (lane - 27 < 0 ? 0 : lane - 27);
+            int st = INT_MAX, len = 0, rank = lane;
             if (lane < 27) {
                 const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
                 int x = cx + dx, y = cy + dy, z = cz + dz;
@@ -250,23 +257,54 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
                 len = st >= cs ? (int)(cstart[cc + 1] - cstart[cc]) : 0;
                 rank = axis_rank3(cx, dx, nc) * 9 + axis_rank3(cy, dy, nc) * 3 + axis_rank3(cz, dz, nc);
             }
-            s_rs[rank] = st;   // lanes 27..31 pad ranks 27..31 with INT_MAX
+            s_rs[rank] = st;
             s_rn[rank] = len;
-            s_rs[32 + (lane & 15)] = INT_MAX;
             __syncwarp();
-            const int myn = s_rn[lane];
-            int incl = myn;
+            // merge the non-empty runs (ascending) into contiguous segments
+            const int st_r = s_rs[lane], len_r = s_rn[lane], end_r = st_r + len_r;
+            const unsigned km = __ballot_sync(0xffffffffu, len_r > 0);
+            const unsigned before = km & lt;
+            const int prev = before ? 31 - __clz(before) : 0;
+            const int prev_end = __shfl_sync(0xffffffffu, end_r, prev);
+            const bool seg = len_r > 0 && (before == 0 || prev_end != st_r);
+            const unsigned sm = __ballot_sync(0xffffffffu, seg);
+            const unsigned above = lane == 31 ? 0u : sm & ~((2u << lane) - 1u);
+            const int nxt = above ? __ffs(above) - 1 : 32;
+            const unsigned kb = km & (nxt >= 32 ? 0xffffffffu : ((1u << nxt) - 1u));
+            const int last = kb ? 31 - __clz(kb) : 0;
+            const int seg_end = __shfl_sync(0xffffffffu, end_r, last);
+            const int seglen = seg ? seg_end - st_r : 0;
+            int incl = seglen;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            s_roff[lane] = incl - myn;
-            if (lane == 31) s_m = incl;
+            const int nseg = __popc(sm);
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if (seg) {
+                const int k = __popc(sm & lt);
+                const int off = incl - seglen;
+                s_ss[k] = st_r;
+                s_soff[k] = off;
+                s_fin[k] = make_int2(seg_end, off - st_r);
+            }
+            __syncwarp();
+            if (lane >= nseg) {
+                s_ss[lane] = INT_MAX;
+                s_soff[lane] = INT_MAX;
+            }
+            s_ss[32 + lane] = INT_MAX;
+            s_soff[32 + lane] = INT_MAX;
+            if (lane == 0) {
+                s_m = total;
+                s_nseg = nseg;
+            }
         }
         __syncthreads();
         const int M = s_m;
         const bool win = M <= kWin;   // (CTA-uniform)
+        const bool small = s_nseg <= 8;
         if (win)
             for (int k = tid; k < M; k += kHalfCellThreads) wx[k] = wy[k] = wz[k] = 0.0;
         __syncthreads();
@@ -324,7 +362,8 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
                         ay = fma(-df, dy_, ay);
                         az = fma(-df, dz_, az);
                         cnt++;
-                        const int sl = win ? win_slot(j[u], s_rs, s_rn, s_roff) : -1;
+                        const int sl = !win ? -1 : (small ? win_slot<3>(j[u], s_ss, s_fin)
+                                                          : win_slot<5>(j[u], s_ss, s_fin));
                         win_add(wx, sl, df * dx_, &p[j[u]].x);
                         win_add(wy, sl, df * dy_, &p[j[u]].y);
                         win_add(wz, sl, df * dz_, &p[j[u]].z);
@@ -334,7 +373,8 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
             unsigned dummy = 0;
             group_reduce<G>(ax, ay, az, dummy);
             if (active && g == 0) {
-                const int sl = win ? win_slot((int)i, s_rs, s_rn, s_roff) : -1;
+                const int sl = !win ? -1 : (small ? win_slot<3>((int)i, s_ss, s_fin)
+                                                  : win_slot<5>((int)i, s_ss, s_fin));
                 win_add(wx, sl, ax, &p[i].x);
                 win_add(wy, sl, ay, &p[i].y);
                 win_add(wz, sl, az, &p[i].z);
@@ -345,13 +385,10 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
             for (int k = tid; k < M; k += kHalfCellThreads) {
                 const double vx = wx[k], vy = wy[k], vz = wz[k];
                 if (vx != 0.0 || vy != 0.0 || vz != 0.0) {
-                    int r = 0;   // largest r with s_roff[r] <= k and a non-empty run
+                    int r = 0;   // the segment holding slot k: largest r with s_soff[r] <= k
 #pragma unroll
-                    for (int st = 16; st > 0; st >>= 1) {
-                        const int rr = r + st;
-                        r = (rr < 27 && s_roff[rr] <= k) ? rr : r;
-                    }
-                    const int64_t a = (int64_t)s_rs[r] + (k - s_roff[r]);
+                    for (int st = 16; st > 0; st >>= 1) r = s_soff[r + st] <= k ? r + st : r;
+                    const int64_t a = (int64_t)s_ss[r] + (k - s_soff[r]);
                     atomicAdd(&p[a].x, vx);
                     atomicAdd(&p[a].y, vy);
                     atomicAdd(&p[a].z, vz);
