@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--order", default=None, choices=["lattice", "shuffled", "cell"],
                     help="storage order; default: config 2 shuffled, 3 cell, 4/5 cell (re-sorted at every rebuild)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--repeats", type=int, default=5,
+                    help="graph step control: time the K steps this many times (min / median reported; "
+                         "the headline value is the first)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every step eagerly (configs 2/3: no force replay; MD configs: host-side step control)")
     ap.add_argument("--no-overlap", action="store_true", help="P > 1: blocking all-gather (no comm/compute overlap)")
@@ -407,6 +410,23 @@ def main():
                 "l1_view": {"lsu_data_pipe_wavefronts_pct_of_peak": l1_pct,
                             "source": f"profiles/traffic_config{args.config}.json (ncu --set full of this kernel)"}}
 
+    # ---- repeats of the timed steps (SURVEY §8(d) timing protocol: min and median) ----
+    repeats = None
+    if md_graph is not None and args.repeats > 1:
+        rms = [ms_max / args.steps]
+        for _ in range(args.repeats - 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            md_graph.launch()
+            b.record(stream)
+            torch.cuda.synchronize()
+            md_graph.finish()
+            rms.append(a.elapsed_time(b) / args.steps)
+        srt = sorted(rms)
+        repeats = {"n": len(rms), "ms_per_step_min": srt[0], "ms_per_step_median": srt[len(srt) // 2],
+                   "note": "repeat 1 is the timed line; later repeats continue the trajectory (more rebuilds "
+                           "may fall in a window)"}
+
     # ---- e2e: same steps through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -525,6 +545,7 @@ def main():
             "step_control": ("device (lj_md_graph: conditional rebuild node, one graph launch for the timed steps)"
                              if md_graph is not None else "host" + graph_note),
             "roofline": roof,
+            "repeats": repeats,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         }
         if energies:
