@@ -307,9 +307,9 @@ def main():
     # (lj_md_graph, device-side decision: no host round trip per step or rebuild)
     md_graph = None
     graph_note = ""
-    if not force_only and not args.no_graph and not sim.collective and every == 0:
+    if not force_only and not args.no_graph and not sim.collective:
         try:
-            md_graph = sim.graph(args.steps)
+            md_graph = sim.graph(args.steps, energy_every=every)
         except lj.LJError as ex:   # e.g. a driver without conditional graph nodes: eager GPU steps
             graph_note = f" (graph unavailable: {ex})"
     lj_graph_launches = [0]
@@ -335,9 +335,10 @@ def main():
     barrier()
     if md_graph is not None:
         graph_rebuilds = md_graph.finish()
-        per_step, per_rebuild = md_graph.g.kernels()
-        lj_graph_launches[0] = per_step * args.steps + per_rebuild * graph_rebuilds
-        f_ms_graph = md_graph.g.force_ms()
+        per_step, per_rebuild = md_graph.g.kernels()   # (all unrolled steps, per rebuild)
+        lj_graph_launches[0] = per_step + per_rebuild * graph_rebuilds
+        f_ms_graph = [t for t in md_graph.g.force_ms() if t > 0]   # sample steps are not timed
+        energies = md_graph.energies()
     launches = lj.launch_count() - launches0 + lj_graph_launches[0]   # graph replays launch without the host
     ck = clocks.stop()
     ms = t0.elapsed_time(t1)

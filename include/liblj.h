@@ -325,6 +325,9 @@ typedef struct {
                                  (the list is then invalid), [2] = entries of the last rebuild */
     int reorder;              /* re-sort into cell order at every rebuild (as lj_rebuild) */
     int steps;                /* steps per launch, 1..100000 (unrolled in the graph) */
+    int energy_every;         /* 0, or sample (KE, PE) at steps k % energy_every == 0 of every launch: the
+                                 kick is split in two halves around lj_energy (reading O8, synchronised p) */
+    double *energies;         /* 2 doubles per sample (ceil(steps / energy_every) samples), if energy_every */
 } lj_md_graph_desc;
 
 typedef struct lj_md_graph lj_md_graph;
@@ -345,8 +348,8 @@ lj_status lj_md_graph_launch(lj_md_graph *gr, void *stream);
 /* After a launch has completed: ms[k] = duration of step k's force kernel (CUDA
  * events recorded around it inside the graph), k < min(n, steps). */
 lj_status lj_md_graph_force_ms(const lj_md_graph *gr, float *ms, int n);
-/* Kernels in one step without / in one rebuild (for launch accounting). */
-lj_status lj_md_graph_kernels(const lj_md_graph *gr, long long *per_step, long long *per_rebuild);
+/* Kernels one launch runs without its rebuilds (all unrolled steps) / per rebuild. */
+lj_status lj_md_graph_kernels(const lj_md_graph *gr, long long *steps_total, long long *per_rebuild);
 lj_status lj_md_graph_destroy(lj_md_graph *gr);
 
 /* Wrap q into [0,L) (x -= L floor(x/L); x -= L if x >= L) for atoms [0,n) and,

@@ -568,8 +568,9 @@ lj_status lj_ipc_close(void* ptr) {
 struct lj_md_graph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    long long kernels_step = 0, kernels_rebuild = 0;
+    long long kernels_steps = 0, kernels_rebuild = 0;   // all unrolled steps (no rebuild) / one rebuild
     std::vector<cudaEvent_t> ev;   // per step: force begin, force end
+    std::vector<char> timed;       // the step's force kernel sits between its two events
 };
 
 lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
@@ -581,6 +582,8 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
     if (n < 1) return fail(LJ_ERR_ARG, "md_graph: n must be >= 1");
     if (d->steps < 1 || d->steps > 100000) return fail(LJ_ERR_ARG, "md_graph: steps must be in [1, 100000]");
     if (!std::isfinite(d->dt)) return fail(LJ_ERR_ARG, "md_graph: dt not finite");
+    if (d->energy_every < 0 || (d->energy_every > 0 && !d->energies))
+        return fail(LJ_ERR_ARG, "md_graph: energy_every needs an energies buffer");
     if (!d->q || !d->p || !d->q_ref || !d->perm || !d->disp || !d->status || !d->number_of_partners || !d->pointer ||
         !d->sorted_list || !d->workspace || (d->reorder && (!d->q_alt || !d->p_alt)))
         return fail(LJ_ERR_ARG, "md_graph: null pointer");
@@ -625,6 +628,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
     const int lanes = n >= 500000 ? (4 | (3 << 8)) : (8 | (2 << 8));   // lj_force_step_ex's defaults
     const size_t rec = sizeof(double) * 4 * (size_t)n;
     gr->ev.resize(2 * (size_t)d->steps, nullptr);
+    gr->timed.assign((size_t)d->steps, 0);
     for (auto& ev : gr->ev) LJ_G(cudaEventCreate(&ev), "md_graph/event");
     cudaGraphNode_t prev = nullptr;
     for (int k = 0; k < d->steps; k++) {
@@ -635,9 +639,23 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
              "md_graph/capture");
         long long l0 = g_launches;
         cudaGraphConditionalHandle h = 0;
-        cudaError_t e = cudaEventRecordWithFlags(gr->ev[2 * k], cs, cudaEventRecordExternal);
-        if (e == cudaSuccess) e = launch_force_full(fa, lanes, cs);
-        if (e == cudaSuccess) e = cudaEventRecordWithFlags(gr->ev[2 * k + 1], cs, cudaEventRecordExternal);
+        cudaError_t e = cudaSuccess;
+        if (d->energy_every > 0 && k % d->energy_every == 0) {
+            // sample step: p_n = p_{n-1/2} + F dt/2, (KE, PE) at the synchronised p, the second half kick
+            ForceArgs half_kick = fa;
+            half_kick.dt = 0.5 * d->dt;
+            e = launch_force_full(half_kick, lanes, cs);
+            if (e == cudaSuccess)
+                e = launch_energy(d->q, d->p, 0, n, d->number_of_partners, d->pointer, d->sorted_list, d->g.L,
+                                  d->g.rc * d->g.rc, d->g.rc, 0, d->energies + 2 * (k / d->energy_every), cs);
+            half_kick.n_inter = nullptr;
+            if (e == cudaSuccess) e = launch_force_full(half_kick, lanes, cs);
+        } else {   // the force kernel between two event nodes: its duration per step
+            e = cudaEventRecordWithFlags(gr->ev[2 * k], cs, cudaEventRecordExternal);
+            if (e == cudaSuccess) e = launch_force_full(fa, lanes, cs);
+            if (e == cudaSuccess) e = cudaEventRecordWithFlags(gr->ev[2 * k + 1], cs, cudaEventRecordExternal);
+            gr->timed[k] = 1;
+        }
         if (e == cudaSuccess) e = launch_integrate_disp(d->q, d->p, d->q_ref, 0, n, d->dt, d->disp, cs);
         if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, gr->graph, 0, cudaGraphCondAssignDefault);
         if (e == cudaSuccess) e = launch_md_decide(d->disp, d->g.rs - d->g.rc, h, d->status, cs);
@@ -651,7 +669,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
         cudaError_t e2 = cudaStreamEndCapture(cs, &tmp);
         LJ_G(e, "md_graph/step");
         LJ_G(e2, "md_graph/capture-end");
-        if (k == 0) gr->kernels_step = g_launches - l0;
+        gr->kernels_steps += g_launches - l0;
         // IF (rebuild): the body is the bookkeeping rebuild, captured into the conditional's graph
         cudaGraphNodeParams cp = {};
         cp.type = cudaGraphNodeTypeConditional;
@@ -694,7 +712,10 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
 
 lj_status lj_md_graph_force_ms(const lj_md_graph* gr, float* ms, int n) {
     if (!gr || !ms || n < 0 || 2 * (size_t)n > gr->ev.size()) return fail(LJ_ERR_ARG, "md_graph_force_ms: bad argument");
-    for (int k = 0; k < n; k++) LJ_CUDA(cudaEventElapsedTime(ms + k, gr->ev[2 * k], gr->ev[2 * k + 1]), "event");
+    for (int k = 0; k < n; k++) {   // sample steps (split kick, no events) report 0
+        ms[k] = 0.0f;
+        if (gr->timed[k]) LJ_CUDA(cudaEventElapsedTime(ms + k, gr->ev[2 * k], gr->ev[2 * k + 1]), "event");
+    }
     return LJ_OK;
 }
 
@@ -706,7 +727,7 @@ lj_status lj_md_graph_launch(lj_md_graph* gr, void* stream) {
 
 lj_status lj_md_graph_kernels(const lj_md_graph* gr, long long* per_step, long long* per_rebuild) {
     if (!gr || !per_step || !per_rebuild) return fail(LJ_ERR_ARG, "md_graph_kernels: null pointer");
-    *per_step = gr->kernels_step;
+    *per_step = gr->kernels_steps;
     *per_rebuild = gr->kernels_rebuild;
     return LJ_OK;
 }

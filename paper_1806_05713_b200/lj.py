@@ -66,7 +66,8 @@ class MDGraphDesc(ctypes.Structure):
                 ("dt", ctypes.c_double), ("number_of_partners", ctypes.c_void_p), ("pointer", ctypes.c_void_p),
                 ("sorted_list", ctypes.c_void_p), ("capacity", ctypes.c_int64), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t), ("disp", ctypes.c_void_p), ("n_interactions", ctypes.c_void_p),
-                ("status", ctypes.c_void_p), ("reorder", ctypes.c_int), ("steps", ctypes.c_int)]
+                ("status", ctypes.c_void_p), ("reorder", ctypes.c_int), ("steps", ctypes.c_int),
+                ("energy_every", ctypes.c_int), ("energies", ctypes.c_void_p)]
 
 
 _lib = None
@@ -371,19 +372,20 @@ class MDGraph:
     decision, conditional rebuild) as one CUDA graph.  Holds references to every buffer."""
 
     def __init__(self, q, p, q_alt, p_alt, q_ref, perm, g: Geom, dt: float, builder: "ListBuilder",
-                 disp, counter, status, reorder: bool, steps: int):
+                 disp, counter, status, reorder: bool, steps: int, energy_every: int = 0, energies=None):
         for t, name in ((q, "q"), (p, "p"), (q_ref, "q_ref")):
             _rec(t, name)
         if not builder.padded:
             raise ValueError("MDGraph: needs the padded list layout")
-        self._keep = (q, p, q_alt, p_alt, q_ref, perm, builder, disp, counter, status)
+        self._keep = (q, p, q_alt, p_alt, q_ref, perm, builder, disp, counter, status, energies)
         self.steps = int(steps)
         d = MDGraphDesc(_ptr(q).value, _ptr(p).value, _ptr(q_alt).value if q_alt is not None else None,
                         _ptr(p_alt).value if p_alt is not None else None, _ptr(q_ref).value, _ptr(perm).value,
                         q.shape[0], g, float(dt), _ptr(builder.npart).value, _ptr(builder.pointer).value,
                         _ptr(builder.sorted_list).value, builder.sorted_list.numel(), _ptr(builder.workspace).value,
                         builder.workspace.numel(), _ptr(disp).value, _ptr(counter).value if counter is not None
-                        else None, _ptr(status).value, int(bool(reorder)), self.steps)
+                        else None, _ptr(status).value, int(bool(reorder)), self.steps, int(energy_every),
+                        _ptr(energies).value if energies is not None else None)
         h = ctypes.c_void_p()
         _check(load().lj_md_graph_create(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
@@ -398,6 +400,7 @@ class MDGraph:
         return list(out)
 
     def kernels(self) -> tuple[int, int]:
+        """(kernels of all unrolled steps without rebuilds, kernels per rebuild)."""
         a, b = ctypes.c_longlong(), ctypes.c_longlong()
         _check(load().lj_md_graph_kernels(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value

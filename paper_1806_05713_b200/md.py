@@ -146,9 +146,17 @@ class StepStats:
 class StepGraph:
     """A LeapfrogMD.graph(): the steps run on the device without host round trips."""
 
-    def __init__(self, sim, g, status):
+    def __init__(self, sim, g, status, energy_every=0, energies=None):
         self.sim, self.g, self.status = sim, g, status
+        self.energy_every, self._energies = energy_every, energies
         self._seen = 0
+
+    def energies(self):
+        """[(step, KE, PE)] of the last completed launch (energy_every > 0; one rank: no reduction)."""
+        if self._energies is None:
+            return []
+        e = self._energies.view(-1, 2).tolist()
+        return [(k * self.energy_every, ke, pe) for k, (ke, pe) in enumerate(e)]
 
     def launch(self):
         self.g.launch()
@@ -497,7 +505,7 @@ class LeapfrogMD:
         return float(out[0]), float(out[1])
 
     # ---- the step as a CUDA graph (NEXT-1: "capture the whole step"; one rank) ----
-    def graph(self, steps: int) -> "StepGraph":
+    def graph(self, steps: int, energy_every: int = 0) -> "StepGraph":
         """The next `steps` leapfrog steps (as step()) as one CUDA graph with a device-side
         rebuild decision (lj_md_graph): launch with .launch(), then .finish() after a
         synchronisation to fold the rebuilds into the driver's state."""
@@ -509,10 +517,12 @@ class LeapfrogMD:
         if getattr(self.be, "perm", None) is None:
             self.be.perm = torch.empty(self.n, dtype=torch.int64, device=self.q.device)
         status = torch.zeros(4, dtype=torch.int64, device=self.q.device)
+        ns = -(-steps // energy_every) if energy_every > 0 else 0
+        energies = torch.zeros(max(2 * ns, 1), dtype=torch.float64, device=self.q.device)
         g = lj.MDGraph(self.q, self.p, self.q_alt if self.reorder else None, self.p_alt if self.reorder else None,
                        self.q_ref, self.be.perm, self.g, self.dt, self.be.builder, self.disp, self.counter, status,
-                       self.reorder, steps)
-        return StepGraph(self, g, status)
+                       self.reorder, steps, energy_every, energies if ns else None)
+        return StepGraph(self, g, status, energy_every, energies if ns else None)
 
     def close(self):
         """Unmap the peers' replicas (exchange="push"); the driver is unusable afterwards."""

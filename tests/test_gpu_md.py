@@ -92,3 +92,35 @@ def test_step_graph_equals_eager_steps(md, reorder):
     gr.finish()
     assert torch.equal(a.q, b.q) and torch.equal(a.p, b.p) and a.stats.rebuilds == b.stats.rebuilds
     gr.close()
+
+
+def test_step_graph_energy_samples(md):
+    """energy_every: the graph splits the kick around lj_energy at sample steps, as the
+    eager driver's bench path does -- same trajectory bit for bit, same energies."""
+    from paper_1806_05713_b200 import lj
+    w = lj_inputs.make_system(10, jitter_seed=1, T=1.0, mom_seed=5, dt=0.005)
+    g = lj.geom(w.L, w.rc, w.rs)
+    dev = torch.device("cuda:0")
+    steps, every = 24, 5
+    a, b = (md.LeapfrogMD(md.LibBackend(w.n, g, 0, w.n, dev), w.q, w.p, g, w.dt) for _ in range(2))
+    ref = []
+    for k in range(steps):
+        if k % every == 0:
+            a.be.force(a.q, a.p, 0.5 * w.dt, a.lst, a.counter)
+            e = a.energy()
+            a.be.force(a.q, a.p, 0.5 * w.dt, a.lst)
+            ref.append((k, e[0], e[1]))
+        else:
+            a.kick(w.dt, a.counter)
+        a.drift_and_exchange()
+    gr = b.graph(steps, energy_every=every)
+    gr.launch()
+    torch.cuda.synchronize()
+    gr.finish()
+    assert torch.equal(a.q, b.q) and torch.equal(a.p, b.p) and a.stats.rebuilds == b.stats.rebuilds
+    got = gr.energies()
+    assert [k for k, _, _ in got] == [k for k, _, _ in ref]
+    assert np.allclose([x[1:] for x in got], [x[1:] for x in ref], rtol=1e-12, atol=0)
+    ms = gr.g.force_ms()
+    assert all((t == 0) == (k % every == 0) for k, t in enumerate(ms))
+    gr.close()
