@@ -155,8 +155,10 @@ lj_status lj_force_step(const double *q, double *p, int64_t n, lj_geom g, double
                         const int32_t *sorted_list, void *stream);
 
 /* Tuning / instrumentation variant of lj_force_step.
- * lanes_per_row: 0 = library default, else one of 1,2,4,8,16,32 threads
- * cooperating on a row.  n_interactions: NULL or a device uint64 to which the
+ * lanes_per_row = G | (U << 8): G (1,2,4,8,16,32) threads cooperate on a row,
+ * U (2,3,4; 0 = 2) partner gathers in flight per thread; 0 = the library
+ * default (G = 4, U = 3 for a full list of >= 500k rows, else G = 8, U = 2).
+ * n_interactions: NULL or a device uint64 to which the
  * number of list entries inside r_c is ADDED (pair interactions; a full list
  * counts each pair twice).  ordered != 0 (full list only): one thread per row,
  * ascending j, the oracle's exact expression order (Alg. 3 accumulating into
