@@ -41,7 +41,8 @@ N_SM = 148
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the config's own, BASELINE.json: 100 for configs 2-4, 1000 for 5)")
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -62,7 +63,10 @@ def parse():
     ap.add_argument("--energy-every", type=int, default=None,
                     help="NVE energy sample interval in timed steps (default: config 5 -> steps/20, else off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = lj_inputs.CONFIGS[a.config]["steps"]
+    return a
 
 
 def peaks():
@@ -133,10 +137,33 @@ class ClockSampler:
 
 # ---- the oracle as the CPU baseline / reference arm ---------------------------------
 
-def oracle_sample(w, steps, frac=8, warmup=0, timings=None):
-    """Oracle (plain C, 1 thread) leapfrog steps on rows [0, N/frac) of the workload:
+# One bounded sample of the workload for every CPU leg (cpu_baseline and --impl reference):
+# rows [0, N/frac) of the config, the oracle's list of those rows built once (untimed).
+SAMPLE_FRAC = {2: 1, 3: 1, 4: 8, 5: 64}
+
+
+def host_info():
+    """Cores this process may use and the host CPU model (the GPU box's host, not the build box)."""
+    cores = len(os.sched_getaffinity(0))
+    model = None
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:  # noqa: BLE001 -- lscpu missing
+        pass
+    return {"cores_available": cores, "cpu_model": model}
+
+
+def oracle_sample(w, steps, frac=8, warmup=0, timings=None, threads=None):
+    """Oracle (plain C) leapfrog steps on rows [0, N/frac) of the workload:
     force + integrate + displacement check per step, list built once (not timed).
-    Returns (pairs/s, seconds, pairs)."""
+    threads=None: the oracle as it stands (1 thread, the paper's protocol, PAPER.md:72);
+    threads=C: the all-core timing build of the full-list force step (OpenMP over rows,
+    bit-identical results).  Returns (pairs/s, seconds, pairs)."""
     import oracle
     rows = w.n // frac
     q = oracle.wrap(w.q, w.L)   # a fresh contiguous copy
@@ -147,7 +174,10 @@ def oracle_sample(w, steps, frac=8, warmup=0, timings=None):
     t_total = 0.0
     for s in range(warmup + steps):
         t0 = time.perf_counter()
-        oracle.force_step(q, p, w.L, w.rc, w.dt, lst, inplace=True)
+        if threads is None:
+            oracle.force_step(q, p, w.L, w.rc, w.dt, lst, inplace=True)
+        else:
+            oracle.force_step_full_rows_parallel(q, p, w.L, w.rc, w.dt, lst, threads=threads)
         oracle.integrate(q, p, w.dt, 0, rows, inplace=True)
         oracle.max_displacement(q, qref, 0, rows)
         dt_s = time.perf_counter() - t0
@@ -165,29 +195,26 @@ def oracle_sample(w, steps, frac=8, warmup=0, timings=None):
     return pairs / t_total, t_total, pairs
 
 
-def cores_used():
-    return 1   # the oracle is single-threaded (PAPER.md:72 protocol)
-
-
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     w = lj_inputs.config(args.config)
-    frac = 64 if args.config == 4 else (512 if args.config == 5 else 4)
+    frac = SAMPLE_FRAC[args.config]
     step_times = []
     t0 = time.perf_counter()
     value, secs, pairs = oracle_sample(w, args.steps, frac=frac, warmup=args.warmup, timings=step_times)
-    sample = (f"config {args.config} rows [0, N/{frac}) = {w.n // frac} of {w.n} atoms; oracle list built once "
-              f"(untimed); {args.steps} timed leapfrog steps (force + integrate + displacement), {args.warmup} warm-up")
+    sample = (f"config {args.config} rows [0, N/{frac}) = {w.n // frac} of {w.n} atoms (the same sample as "
+              f"cpu_baseline); oracle list built once (untimed); {args.steps} timed leapfrog steps "
+              f"(force + integrate + displacement), {args.warmup} warm-up")
     line = {
         "impl": "reference", "metric": METRIC, "value": value / 1e9, "unit": "G pair-interactions/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config{args.config}", "n_atoms": w.n, "sample_rows": w.n // frac},
-        "cpu_baseline": {"value": value / 1e9, "unit": "G pair-interactions/s", "cores": cores_used(),
-                         "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value / 1e9, "unit": "G pair-interactions/s", "cores": 1,
+                         "kind": "oracle", "sample": sample, "host": host_info()},
         "e2e": {"value": value / 1e9, "unit": "G pair-interactions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t0,
@@ -196,6 +223,25 @@ def run_reference(args):
 
 
 # ---- our arm ----------------------------------------------------------------------
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` launched as a single process: re-execute it as N ranks, one
+    per GPU, under torch.distributed.run (the driver's own launch line).  Fails loudly
+    if fewer than N GPUs are visible -- never silently times one rank."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        raise SystemExit(f"bench.py --gpus {n}: only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
 
 def main():
     args = parse()
@@ -209,7 +255,11 @@ def main():
     from paper_1806_05713_b200 import lj, md
 
     lj.load()   # fails loudly without the CUDA library
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args.gpus)   # re-executes this command under torchrun (never returns)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
@@ -515,12 +565,20 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # ~10 s of single-thread oracle work (the contract's 10-30 s bounded sample)
-        frac, nst = {4: (8, 30), 5: (64, 30)}.get(args.config, (1, 30))
+        # ~10 s of single-thread oracle work (the contract's 10-30 s bounded sample), on the same
+        # sample the --impl reference arm times; then the all-core OpenMP timing build on it
+        frac, nst = SAMPLE_FRAC[args.config], 30
         v, secs, _ = oracle_sample(w, nst, frac=frac)
-        cpu = {"value": v / 1e9, "unit": "G pair-interactions/s", "cores": cores_used(), "kind": "oracle",
+        hi = host_info()
+        cpu = {"value": v / 1e9, "unit": "G pair-interactions/s", "cores": 1, "kind": "oracle",
                "sample": f"config {args.config} rows [0,N/{frac}) ({w.n // frac} atoms), {nst} oracle leapfrog steps "
-                         f"(force+integrate+displacement; list built once, untimed, not rebuilt), {secs:.1f} s"}
+                         f"(force+integrate+displacement; list built once, untimed, not rebuilt), {secs:.1f} s",
+               "host": hi}
+        if not half:
+            nth = hi["cores_available"]
+            va, secs_a, _ = oracle_sample(w, nst, frac=frac, threads=nth)
+            cpu["all_core"] = {"value": va / 1e9, "cores": nth, "seconds": secs_a,
+                               "kind": "oracle all-core timing build (OpenMP over full-list rows, bit-identical)"}
 
     if rank == 0:
         line = {

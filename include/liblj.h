@@ -154,15 +154,24 @@ lj_status lj_force_step(const double *q, double *p, int64_t n, lj_geom g, double
                         const int32_t *number_of_partners, const int64_t *pointer,
                         const int32_t *sorted_list, void *stream);
 
+/* lanes_per_row flag: the list indices are read V = U (2 or 4) at a time with
+ * one 64/128-bit load per thread (fewer L1 requests for the index stream). */
+#define LJ_LANES_IDXV (1 << 16)
+
 /* Tuning / instrumentation variant of lj_force_step.
- * lanes_per_row = G | (U << 8): G (1,2,4,8,16,32) threads cooperate on a row,
- * U (2,3,4; 0 = 2) partner gathers in flight per thread; 0 = the library
- * default (G = 4, U = 3 for a full list of >= 500k rows, else G = 8, U = 2).
+ * lanes_per_row = G | (U << 8) [| LJ_LANES_IDXV]: G (1,2,4,8,16,32) threads
+ * cooperate on a row, U (2,3,4; 0 = 2) partner gathers in flight per thread;
+ * with LJ_LANES_IDXV, G in (1,2,4,8,16) and U in (2,4) is the index vector
+ * width.  0 = the library default (lj_default_lanes).
  * n_interactions: NULL or a device uint64 to which the
  * number of list entries inside r_c is ADDED (pair interactions; a full list
  * counts each pair twice).  ordered != 0 (full list only): one thread per row,
  * ascending j, the oracle's exact expression order (Alg. 3 accumulating into
  * the loaded p_i, IEEE division, no FMA) -- bit-identical to the oracle. */
+/* The lanes_per_row lj_force_step uses for `rows` rows of a full (half = 0) or
+ * half list (the round-2 sweeps). */
+int lj_default_lanes(int64_t rows, int half);
+
 lj_status lj_force_step_ex(const double *q, double *p, int64_t n, lj_geom g, double dt, int half,
                            int64_t row_begin, int64_t row_end,
                            const int32_t *number_of_partners, const int64_t *pointer,

@@ -32,6 +32,44 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+_LIB_OMP = os.path.join(_HERE, "liblj_oracle_omp.so")
+_lib_omp = None
+
+
+def build_omp(force: bool = False) -> str:
+    """liblj_oracle_omp.so: the same source with -fopenmp, for the all-core timing leg only."""
+    if force or not os.path.exists(_LIB_OMP) or os.path.getmtime(_LIB_OMP) < os.path.getmtime(_SRC):
+        tmp = _LIB_OMP + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-fopenmp", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_OMP)
+    return _LIB_OMP
+
+
+def force_step_full_rows_parallel(q, p, L, rc, dt, csr: "CSR", threads: int | None = None):
+    """All-core timing of the full-list force step (bit-identical to force_step; never
+    used for parity).  p is updated in place (float64, C-contiguous); returns the
+    number of OpenMP threads used."""
+    global _lib_omp
+    if _lib_omp is None:
+        build_omp()
+        L_ = ctypes.CDLL(_LIB_OMP)
+        d, i64, vp = ctypes.c_double, ctypes.c_int64, ctypes.c_void_p
+        L_.lj_oracle_force_step_full_rows_parallel.restype = None
+        L_.lj_oracle_force_step_full_rows_parallel.argtypes = [vp, vp, i64, d, d, d, i64, i64, vp, vp, vp]
+        L_.omp_set_num_threads.argtypes = [ctypes.c_int]
+        L_.omp_get_max_threads.restype = ctypes.c_int
+        _lib_omp = L_
+    if csr.half:
+        raise ValueError("force_step_full_rows_parallel: full lists only")
+    assert q.dtype == np.float64 and q.flags.c_contiguous and p.dtype == np.float64 and p.flags.c_contiguous
+    if threads is not None:
+        _lib_omp.omp_set_num_threads(int(threads))
+    _lib_omp.lj_oracle_force_step_full_rows_parallel(_p(q), _p(p), q.shape[0], L, rc, dt, csr.row_begin,
+                                                     csr.row_end, _p(csr.number_of_partners), _p(csr.pointer),
+                                                     _p(csr.sorted_list))
+    return int(_lib_omp.omp_get_max_threads())
+
+
 def lib():
     global _lib
     if _lib is None:

@@ -335,6 +335,45 @@ void lj_oracle_force_step(const double *q, double *p, int64_t n, double L, doubl
     }
 }
 
+/* All-core TIMING build only (SURVEY §8(d) "an optional OpenMP
+ * full-list build on all cores"): lj_oracle_force_step for a FULL list with the
+ * rows split over OpenMP threads.  Full-list rows are independent (no p_j
+ * writes), so every row runs exactly the arithmetic, in exactly the order, of
+ * lj_oracle_force_step -- the results are bit-identical (tests/test_oracle_force.py).
+ * Built without -fopenmp (liblj_oracle.so) the pragma is ignored; the bench's
+ * all-core leg loads liblj_oracle_omp.so (-fopenmp).  Never used for parity. */
+void lj_oracle_force_step_full_rows_parallel(const double *q, double *p, int64_t n, double L, double rc, double dt,
+                                             int64_t row_begin, int64_t row_end,
+                                             const int32_t *number_of_partners, const int64_t *pointer,
+                                             const int32_t *sorted_list)
+{
+    const double rc2 = rc * rc;
+    int64_t i;
+    (void)n;
+#pragma omp parallel for schedule(static)
+    for (i = row_begin; i < row_end; i++) {
+        const double *qi = &q[3 * i];
+        double r[3];
+        double pix = p[3 * i + 0], piy = p[3 * i + 1], piz = p[3 * i + 2];
+        int64_t beg = pointer[i - row_begin];
+        int64_t cnt = number_of_partners[i - row_begin];
+        int64_t k;
+        for (k = beg; k < beg + cnt; k++) {
+            int64_t j = sorted_list[k];
+            double r2 = relative(qi, &q[3 * j], L, r);
+            if (r2 < rc2) {
+                double df = impulse_coefficient(r2, dt);
+                pix = pix - df * r[0];
+                piy = piy - df * r[1];
+                piz = piz - df * r[2];
+            }
+        }
+        p[3 * i + 0] = pix;
+        p[3 * i + 1] = piy;
+        p[3 * i + 2] = piz;
+    }
+}
+
 /* The plain definition without any list: for every unordered pair i < j with
  * r2 < rc2 (canonical double loop), Alg. 1 with the sign fix. */
 void lj_oracle_force_brute(const double *q, double *p, int64_t n, double L, double rc, double dt)

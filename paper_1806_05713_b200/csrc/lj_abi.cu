@@ -279,6 +279,12 @@ lj_status lj_permute_rows(const double* in, double* out, const int64_t* perm, in
     return LJ_OK;
 }
 
+int lj_default_lanes(int64_t rows, int half) {
+    // round-1 sweeps (profiles/r01_sweep_*.jsonl, tools/gu_sweep.py): config 4 G4/U3 0.766 ms, G4/U2 0.783 ms
+    const bool big = !half && rows >= 500000;
+    return big ? (4 | (3 << 8)) : (8 | (2 << 8));
+}
+
 lj_status lj_force_step_ex(const double* q, double* p, int64_t n, lj_geom g, double dt, int half, int64_t row_begin,
                            int64_t row_end, const int32_t* number_of_partners, const int64_t* pointer,
                            const int32_t* sorted_list, int lanes_per_row, int ordered,
@@ -294,18 +300,18 @@ lj_status lj_force_step_ex(const double* q, double* p, int64_t n, lj_geom g, dou
     if (rows > 0 && (!q || !p || !number_of_partners || !pointer))
         return fail(LJ_ERR_ARG, "force: null pointer");
     if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "force: q/p not 32-byte aligned");
-    int lanes = lanes_per_row & 0xff, unroll = lanes_per_row >> 8;
-    if (lanes == 0) {   // defaults from the round-1 sweeps (profiles/r01_sweep_*.jsonl, tools/gu_sweep.py)
-        const int64_t rows_ = row_end - row_begin;
-        const bool big = !half && rows_ >= 500000;
-        lanes = big ? 4 : 8;
-        if (unroll == 0) unroll = big ? 3 : 2;   // config 4: G4/U3 0.766 ms, G4/U2 0.783 ms
-    }
-    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
-        return fail(LJ_ERR_ARG, "force: lanes_per_row must be 0,1,2,4,8,16 or 32 (got %d)", lanes_per_row);
-    if (unroll != 0 && unroll != 2 && unroll != 3 && unroll != 4)
-        return fail(LJ_ERR_ARG, "force: unroll (lanes_per_row >> 8) must be 0, 2, 3 or 4 (got %d)", unroll);
-    lanes |= unroll << 8;
+    if (lanes_per_row & ~(0xffff | LJ_LANES_IDXV))
+        return fail(LJ_ERR_ARG, "force: unknown lanes_per_row bits 0x%x", lanes_per_row);
+    if ((lanes_per_row & 0xff) == 0) lanes_per_row = lj_default_lanes(row_end - row_begin, half);
+    int lanes = lanes_per_row & 0xff, unroll = (lanes_per_row >> 8) & 0xff;
+    const int idxv = lanes_per_row & LJ_LANES_IDXV;
+    if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && (lanes != 32 || idxv))
+        return fail(LJ_ERR_ARG, "force: lanes_per_row G must be 1,2,4,8,16 or 32 (not 32 with LJ_LANES_IDXV) (got %d)",
+                    lanes_per_row);
+    if (idxv ? (unroll != 2 && unroll != 4) : (unroll != 0 && unroll != 2 && unroll != 3 && unroll != 4))
+        return fail(LJ_ERR_ARG, "force: unroll (lanes_per_row >> 8) must be 0, 2, 3 or 4 (2 or 4 with "
+                    "LJ_LANES_IDXV) (got %d)", unroll);
+    lanes |= unroll << 8 | idxv;
     ForceArgs a;
     a.q = q;
     a.p = p;
@@ -420,14 +426,10 @@ lj_status lj_gather_probe(const double* q, int64_t n, int64_t row_begin, int64_t
     if (!sink || (row_end > row_begin && (!q || !number_of_partners || !pointer)))
         return fail(LJ_ERR_ARG, "gather_probe: null pointer");
     if (!aligned32(q)) return fail(LJ_ERR_ARG, "gather_probe: q not 32-byte aligned");
-    // same encoding and defaults as lj_force_step_ex on a full list: G | (U << 8)
-    const bool big = (row_end - row_begin) >= 500000;
-    int lanes = lanes_per_row & 0xff, unroll = lanes_per_row >> 8;
-    if (lanes == 0) lanes = big ? 4 : 8;
-    if (unroll == 0) unroll = (big && (lanes_per_row & 0xff) == 0) ? 3 : 2;
-    if (!((lanes == 4 || lanes == 8) && (unroll == 2 || unroll == 3)) && !(lanes == 16 && unroll == 2))
-        return fail(LJ_ERR_ARG, "gather_probe: unsupported lanes_per_row 0x%x", lanes_per_row);
-    lanes |= unroll << 8;
+    // same encoding and defaults as lj_force_step_ex on a full list: G | (U << 8) [| LJ_LANES_IDXV]
+    if ((lanes_per_row & 0xff) == 0) lanes_per_row = lj_default_lanes(row_end - row_begin, 0);
+    int lanes = lanes_per_row;
+    if (((lanes >> 8) & 0xff) == 0) lanes |= 2 << 8;
     ForceArgs a;
     a.q = q;
     a.p = nullptr;
@@ -440,7 +442,9 @@ lj_status lj_gather_probe(const double* q, int64_t n, int64_t row_begin, int64_t
     a.rc2 = 0;
     a.dt = 0;
     a.n_inter = nullptr;
-    LJ_CUDA(launch_gather_probe(a, lanes, sink, (cudaStream_t)stream), "lj_gather_probe");
+    const cudaError_t e = launch_gather_probe(a, lanes, sink, (cudaStream_t)stream);
+    if (e == cudaErrorInvalidValue) return fail(LJ_ERR_ARG, "gather_probe: unsupported lanes_per_row 0x%x", lanes_per_row);
+    LJ_CUDA(e, "lj_gather_probe");
     return LJ_OK;
 }
 
@@ -625,7 +629,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
     fa.rc2 = d->g.rc * d->g.rc;
     fa.dt = d->dt;
     fa.n_inter = d->n_interactions;
-    const int lanes = n >= 500000 ? (4 | (3 << 8)) : (8 | (2 << 8));   // lj_force_step_ex's defaults
+    const int lanes = lj_default_lanes(n, 0);   // lj_force_step_ex's defaults
     const size_t rec = sizeof(double) * 4 * (size_t)n;
     gr->ev.resize(2 * (size_t)d->steps, nullptr);
     gr->timed.assign((size_t)d->steps, 0);

@@ -37,6 +37,7 @@ constexpr int kForceThreads = 256;
 struct PairConsts {
     double L;        // box side (0 = open)
     double c48, c24; // 48 dt, 24 dt
+    double rc2;      // r_c^2 = rc*rc (the oracle's constant)
     long long rc2_bits;
     int hi_halfL;    // high word of L/2 (INT_MAX for open boundaries)
     int hi_L2q;      // high word of (L/2)^2: r^2 below it needs no image (INT_MAX for open boundaries)
@@ -47,6 +48,39 @@ __device__ __forceinline__ double fast_rcp(double x) {
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = fma(-x, y, 1.0);
     return fma(y, fma(e, e, e), y);
+}
+
+// The cutoff test on the oracle's r^2 (readings O3/C-4: r2 = (dx*dx + dy*dy) + dz*dz
+// without FMA, interact iff r2 < rc2).  The kernels evaluate r^2 with FMAs
+// (fma(dz, dz, fma(dy, dy, dx*dx))), which differs from the oracle's rounding by
+// at most ~3 ulp; within kCutBand ulp of rc2 the decision is retaken on the
+// oracle's expression (explicit _rn operations), so the set of interacting pairs
+// is the oracle's bit for bit.  The band is hit by ~1e-13 of the entries of the
+// workloads (rare, divergent path).
+constexpr long long kCutBand = 64;
+__device__ __forceinline__ bool inside_cutoff(double r2, double dx, double dy, double dz, const PairConsts& c) {
+    const long long d = __double_as_longlong(r2) - c.rc2_bits;
+    if ((unsigned long long)(d + kCutBand) > (unsigned long long)(2 * kCutBand)) return d < 0;
+    const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    return r2e < c.rc2;
+}
+// The same for U entries at once: the common decision on the bits, the exact
+// re-evaluation in one rarely taken block (keeps the hot loop's registers).
+template <int U>
+__device__ __forceinline__ void inside_cutoff_u(bool (&in)[U], const int (&j)[U], const double (&r2)[U],
+                                                const double (&dx)[U], const double (&dy)[U], const double (&dz)[U],
+                                                const PairConsts& c) {
+    bool near = false;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const long long d = __double_as_longlong(r2[u]) - c.rc2_bits;
+        in[u] = j[u] >= 0 && d < 0;
+        near |= (unsigned long long)(d + kCutBand) <= (unsigned long long)(2 * kCutBand);
+    }
+    if (__builtin_expect(near, 0)) {
+#pragma unroll
+        for (int u = 0; u < U; u++) in[u] = j[u] >= 0 && inside_cutoff(r2[u], dx[u], dy[u], dz[u], c);
+    }
 }
 
 // Periodic image shift of a raw difference: +-L when |d| > L/2 (decided on the
@@ -129,11 +163,13 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
             hmax = max(hmax, __double2hiint(r2[u]));
         }
         auto accumulate = [&]() {
+            bool inr[U];
+            inside_cutoff_u<U>(inr, j, r2, dx, dy, dz, c);
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const double inv2 = fast_rcp(r2[u]);
                 const double inv6 = inv2 * inv2 * inv2;
-                const bool in = j[u] >= 0 && __double_as_longlong(r2[u]) < c.rc2_bits;
+                const bool in = inr[u];
                 const double df = in ? fma(c.c48, inv6, -c.c24) * (inv6 * inv2) : 0.0;
                 ax = fma(-df, dx[u], ax);
                 ay = fma(-df, dy[u], ay);
@@ -175,6 +211,142 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
             pi.y += ay;
             pi.z += az;
             p[i] = pi;   // pad preserved (read back unchanged)
+        }
+    }
+    count_interactions(cnt, n_inter);
+}
+
+// ---- vectorised index stream (lanes_per_row | LJ_LANES_IDXV) ---------------
+// As k_force, but every lane loads V consecutive list entries with ONE vector
+// load (V = 2: 64-bit, V = 4: 128-bit) and keeps their V gathers in flight.  In
+// k_force a warp's index load covers 32 entries of 32/G rows (one 32-bit load
+// per lane, ~10 L1 tag lookups per instruction); here it covers 32 V entries,
+// cutting the index stream's share of the L1 data-pipe wavefronts -- the
+// resource that binds the kernel (profiles/r01_ncu_force_v12.txt) -- by ~V.
+// The row is read through the V-aligned window that contains it: window slot s
+// holds list[base + s], base = pointer[r] rounded down to a multiple of V, and
+// the row's entries are slots [off, off + n), off = pointer[r] - base.  A lane's
+// vector load stays inside one V*4-byte aligned segment that holds at least one
+// entry of the row, so it never leaves the list's allocation.  Padded lists
+// (pointer = r * 196) have off = 0.
+template <int V>
+struct IdxVec;
+template <>
+struct IdxVec<2> {
+    __device__ static void load(const int32_t* a, int (&j)[2]) {
+        const int2 v = __ldg(reinterpret_cast<const int2*>(a));
+        j[0] = v.x, j[1] = v.y;
+    }
+};
+template <>
+struct IdxVec<4> {
+    __device__ static void load(const int32_t* a, int (&j)[4]) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(a));
+        j[0] = v.x, j[1] = v.y, j[2] = v.z, j[3] = v.w;
+    }
+};
+
+template <int G, int V, bool HALF>
+__global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
+    k_force_idxv(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
+                 const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
+                 PairConsts c, unsigned long long* n_inter) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    const bool active = r < rows;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    unsigned cnt = 0;
+    const int64_t i = row_begin + (active ? r : 0);
+    const rec4 qi = load_rec(q, i);
+    int64_t base = 0;
+    int off = 0, end = 0;
+    if (active) {
+        const int64_t p0 = ptr[r];
+        base = p0 & ~(int64_t)(V - 1);
+        off = (int)(p0 - base);
+        end = off + npart[r];
+    }
+    const int32_t* __restrict__ win = list + base;
+    // software pipeline: the next chunk's index vector is loaded before this chunk's records are used
+    int jn[V];
+    if (V * g < end) {
+        IdxVec<V>::load(win + V * g, jn);
+    } else {
+#pragma unroll
+        for (int u = 0; u < V; u++) jn[u] = -1;
+    }
+    for (int s0 = V * g; __any_sync(0xffffffffu, s0 < end); s0 += V * G) {
+        int j[V];
+        rec4 qj[V];
+#pragma unroll
+        for (int u = 0; u < V; u++) {
+            j[u] = (s0 + u >= off && s0 + u < end) ? jn[u] : -1;
+            qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);   // no entry: r = 0, masked below
+        }
+        const int sn = s0 + V * G;
+        if (sn < end) {
+            IdxVec<V>::load(win + sn, jn);
+        } else {
+#pragma unroll
+            for (int u = 0; u < V; u++) jn[u] = -1;
+        }
+        double dx[V], dy[V], dz[V], r2[V];
+        int hmax = 0;
+#pragma unroll
+        for (int u = 0; u < V; u++) {
+            dx[u] = qj[u].x - qi.x;
+            dy[u] = qj[u].y - qi.y;
+            dz[u] = qj[u].z - qi.z;
+            r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+            hmax = max(hmax, __double2hiint(r2[u]));
+        }
+        auto accumulate = [&]() {
+            bool inr[V];
+            inside_cutoff_u<V>(inr, j, r2, dx, dy, dz, c);
+#pragma unroll
+            for (int u = 0; u < V; u++) {
+                const double inv2 = fast_rcp(r2[u]);
+                const double inv6 = inv2 * inv2 * inv2;
+                const bool in = inr[u];
+                const double df = in ? fma(c.c48, inv6, -c.c24) * (inv6 * inv2) : 0.0;
+                ax = fma(-df, dx[u], ax);
+                ay = fma(-df, dy[u], ay);
+                az = fma(-df, dz[u], az);
+                cnt += in;
+                if (HALF && in) {
+                    atomicAdd(&p[j[u]].x, df * dx[u]);
+                    atomicAdd(&p[j[u]].y, df * dy[u]);
+                    atomicAdd(&p[j[u]].z, df * dz[u]);
+                }
+            }
+        };
+        if (__any_sync(0xffffffffu, hmax >= c.hi_L2q)) {   // some pair may need a periodic image
+#pragma unroll
+            for (int u = 0; u < V; u++) {
+                dx[u] -= image_shift(dx[u], c.L, c.hi_halfL);
+                dy[u] -= image_shift(dy[u], c.L, c.hi_halfL);
+                dz[u] -= image_shift(dz[u], c.L, c.hi_halfL);
+                r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
+            }
+            accumulate();
+        } else {
+            accumulate();
+        }
+    }
+    unsigned cnt_row = cnt;
+    group_reduce<G>(ax, ay, az, cnt_row);
+    if (active && g == 0) {
+        if (HALF) {
+            atomicAdd(&p[i].x, ax);
+            atomicAdd(&p[i].y, ay);
+            atomicAdd(&p[i].z, az);
+        } else {
+            rec4 pi = p[i];
+            pi.x += ax;
+            pi.y += ay;
+            pi.z += az;
+            p[i] = pi;
         }
     }
     count_interactions(cnt, n_inter);
@@ -353,7 +525,7 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const double dx_ = dx[u], dy_ = dy[u], dz_ = dz[u];
-                    const bool in = j[u] >= 0 && __double_as_longlong(r2[u]) < c.rc2_bits;
+                    const bool in = j[u] >= 0 && inside_cutoff(r2[u], dx[u], dy[u], dz[u], c);
                     if (in) {
                         const double inv2 = fast_rcp(r2[u]);
                         const double inv6 = inv2 * inv2 * inv2;
@@ -502,11 +674,13 @@ __global__ void __launch_bounds__(kForceThreads, (LAYOUT == LJ_LAYOUT_SOA || LAY
                 r2[u] = fma(dz[u], dz[u], fma(dy[u], dy[u], dx[u] * dx[u]));
             }
         }
+        bool inr[U];
+        inside_cutoff_u<U>(inr, j, r2, dx, dy, dz, c);
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const double inv2 = inv_r2<RCP>(r2[u]);
             const double inv6 = inv2 * inv2 * inv2;
-            const bool in = j[u] >= 0 && __double_as_longlong(r2[u]) < c.rc2_bits;
+            const bool in = inr[u];
             const double df = in ? fma(c.c48, inv6, -c.c24) * (inv6 * inv2) : 0.0;
             ax = fma(-df, dx[u], ax);
             ay = fma(-df, dy[u], ay);
@@ -557,6 +731,54 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
         }
 #pragma unroll
         for (int u = 0; u < U; u++) s += j[u] >= 0 ? qj[u].x + qj[u].y + qj[u].z : 0.0;
+    }
+    if (s == 1.2345678e300) sink[0] = s;   // never true: keeps the loads alive
+}
+
+// The same probe for the vectorised index stream of k_force_idxv (V entries per index load).
+template <int G, int V>
+__global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
+    k_gather_probe_idxv(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
+                        const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* sink) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    const bool active = r < rows;
+    const int64_t i = active ? r : 0;
+    int64_t base = 0;
+    int off = 0, end = 0;
+    if (active) {
+        const int64_t p0 = ptr[r];
+        base = p0 & ~(int64_t)(V - 1);
+        off = (int)(p0 - base);
+        end = off + npart[r];
+    }
+    const int32_t* __restrict__ win = list + base;
+    double s = 0.0;
+    int jn[V];
+    if (V * g < end) {
+        IdxVec<V>::load(win + V * g, jn);
+    } else {
+#pragma unroll
+        for (int u = 0; u < V; u++) jn[u] = -1;
+    }
+    for (int s0 = V * g; __any_sync(0xffffffffu, s0 < end); s0 += V * G) {
+        int j[V];
+        rec4 qj[V];
+#pragma unroll
+        for (int u = 0; u < V; u++) {
+            j[u] = (s0 + u >= off && s0 + u < end) ? jn[u] : -1;
+            qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);
+        }
+        const int sn = s0 + V * G;
+        if (sn < end) {
+            IdxVec<V>::load(win + sn, jn);
+        } else {
+#pragma unroll
+            for (int u = 0; u < V; u++) jn[u] = -1;
+        }
+#pragma unroll
+        for (int u = 0; u < V; u++) s += j[u] >= 0 ? qj[u].x + qj[u].y + qj[u].z : 0.0;
     }
     if (s == 1.2345678e300) sink[0] = s;   // never true: keeps the loads alive
 }
@@ -619,6 +841,7 @@ PairConsts make_consts(const ForceArgs& a) {
     } u;
     u.d = a.rc2;
     c.rc2_bits = u.b;
+    c.rc2 = a.rc2;
     if (a.L > 0.0) {
         u.d = 0.5 * a.L;
         c.hi_halfL = (int)(u.b >> 32);
@@ -656,13 +879,43 @@ cudaError_t launch_g(const ForceArgs& a, int lanes, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <bool HALF, int V>
+cudaError_t launch_idxv(const ForceArgs& a, int G, cudaStream_t s) {
+    if (a.rows <= 0) return cudaSuccess;
+    PairConsts c = make_consts(a);
+    const int64_t threads = a.rows * (int64_t)G;
+    const unsigned grid = (unsigned)((threads + kForceThreads - 1) / kForceThreads);
+    const rec4* q = (const rec4*)a.q;
+    rec4* p = (rec4*)a.p;
+#define LJ_LAUNCH(GG)                                                                                         \
+    k_force_idxv<GG, V, HALF><<<grid, kForceThreads, 0, s>>>(q, p, a.row_begin, a.rows, a.npart, a.ptr, a.list, c, \
+                                                           a.n_inter)
+    switch (G) {
+        case 1: LJ_LAUNCH(1); break;
+        case 2: LJ_LAUNCH(2); break;
+        case 4: LJ_LAUNCH(4); break;
+        case 8: LJ_LAUNCH(8); break;
+        case 16: LJ_LAUNCH(16); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef LJ_LAUNCH
+    g_launches++;
+    return cudaGetLastError();
+}
+
 }  // namespace
 
-// lanes encodes G (1..32) and, in its upper bits, the unroll U (lanes = G | (U << 8); U in {2, 4}, default 2).
+// lanes encodes G (1..32) and, in its upper bits, the unroll U (lanes = G | (U << 8); U in {2, 3, 4},
+// default 2); with LJ_LANES_IDXV set, U in {2, 4} is the index vector width of k_force_idxv.
 template <bool HALF>
 cudaError_t launch_gu(const ForceArgs& a, int lanes, cudaStream_t s) {
-    const int U = lanes >> 8;
+    const int U = (lanes >> 8) & 0xff;
     const int G = lanes & 0xff;
+    if (lanes & LJ_LANES_IDXV) {
+        if (U == 4) return launch_idxv<HALF, 4>(a, G, s);
+        if (U == 2) return launch_idxv<HALF, 2>(a, G, s);
+        return cudaErrorInvalidValue;
+    }
     if (U == 4) return launch_g<HALF, 4>(a, G, s);
     if (U == 3) return launch_g<HALF, 3>(a, G, s);
     if (U == 0 || U == 2) return launch_g<HALF, 2>(a, G, s);
@@ -677,8 +930,9 @@ cudaError_t launch_force_half_cells(const ForceArgs& a, const int64_t* cstart, i
     const int64_t ncell = (int64_t)nc * nc * nc;
     PairConsts c = make_consts(a);
     const size_t smem = sizeof(double) * 3 * kWin;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)std::min<int64_t>(ncell, (int64_t)sms * (1024 / LJ_HC_THREADS) * 8);
     const rec4* q = (const rec4*)a.q;
     rec4* p = (rec4*)a.p;
@@ -702,7 +956,21 @@ cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cud
     const unsigned grid = (unsigned)((a.rows * (int64_t)(lanes & 0xff) + kForceThreads - 1) / kForceThreads);
     const rec4* q = (const rec4*)a.q;
 #define LJ_PROBE(G, U) k_gather_probe<G, U><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink)
+#define LJ_PROBEV(G, V) \
+    k_gather_probe_idxv<G, V><<<grid, kForceThreads, 0, s>>>(q, a.rows, a.npart, a.ptr, a.list, sink)
     switch (lanes) {
+        case 2 | (2 << 8) | LJ_LANES_IDXV: LJ_PROBEV(2, 2); break;
+        case 4 | (2 << 8) | LJ_LANES_IDXV: LJ_PROBEV(4, 2); break;
+        case 8 | (2 << 8) | LJ_LANES_IDXV: LJ_PROBEV(8, 2); break;
+        case 2 | (4 << 8) | LJ_LANES_IDXV: LJ_PROBEV(2, 4); break;
+        case 4 | (4 << 8) | LJ_LANES_IDXV: LJ_PROBEV(4, 4); break;
+        case 8 | (4 << 8) | LJ_LANES_IDXV: LJ_PROBEV(8, 4); break;
+        case 16 | (4 << 8) | LJ_LANES_IDXV: LJ_PROBEV(16, 4); break;
+        case 2 | (2 << 8): LJ_PROBE(2, 2); break;
+        case 2 | (3 << 8): LJ_PROBE(2, 3); break;
+        case 8 | (4 << 8): LJ_PROBE(8, 4); break;
+        case 4 | (4 << 8): LJ_PROBE(4, 4); break;
+        case 16 | (3 << 8): LJ_PROBE(16, 3); break;
         case 4 | (2 << 8): LJ_PROBE(4, 2); break;
         case 4 | (3 << 8): LJ_PROBE(4, 3); break;
         case 8 | (2 << 8): LJ_PROBE(8, 2); break;
@@ -711,6 +979,7 @@ cudaError_t launch_gather_probe(const ForceArgs& a, int lanes, double* sink, cud
         default: return cudaErrorInvalidValue;
     }
 #undef LJ_PROBE
+#undef LJ_PROBEV
     g_launches++;
     return cudaGetLastError();
 }

@@ -286,6 +286,9 @@ struct ListArgs {
     int32_t* out;             // scratch [rows * kRowCap] or list
     int32_t* overflow_cells;  // cells with more than kMaxCand candidates
     int32_t* n_overflow;      // [0] = #overflow cells, [1] = row overflow flag
+    int clamp;                // out is the caller's padded list: a row over kRowCap stores
+                              // min(count, kRowCap) in npart (consumers stay in bounds until
+                              // the overflow flag is seen); scratch mode keeps the true count
     // v4 (fast path, wrapped input only)
     const rec4* q;            // raw input positions (atom order): the exact band test
     const int32_t* flags;     // [0] != 0: some coordinate outside [0, L) -> exact kernel instead
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
                 cursor += __popc(msk);
             }
             if (lane == 0 && !DIRECT) {
-                a.npart[r] = cursor;
+                a.npart[r] = (a.clamp && cursor > kRowCap) ? kRowCap : cursor;
                 if (cursor > kRowCap) atomicOr(&a.n_overflow[1], 1);
             }
         }
@@ -901,7 +904,8 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
 #pragma unroll
                 for (int r = 0; r < kItemRows; r++) {
                     if (r < nr && lane == r) {
-                        a.npart[__float_as_int(ri[r].w) - a.row_begin] = cur[r];
+                        a.npart[__float_as_int(ri[r].w) - a.row_begin] =
+                            (a.clamp && cur[r] > kRowCap) ? kRowCap : cur[r];
                         if (cur[r] > kRowCap) atomicOr(&a.n_overflow[1], 1);
                     }
                 }
@@ -953,15 +957,18 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_fallback(ListArgs a) {
                 }
             }
             __syncwarp();
-            if (cursor <= kRowBuf) {
-                const int P = next_pow2(cursor > 0 ? cursor : 1);
-                for (int k = cursor + lane; k < P; k += 32) buf[k] = INT_MAX;
+            if (cursor <= kRowBuf || !DIRECT) {
+                // (not DIRECT and cursor > kRowBuf: the row overflows the stride anyway; the
+                // first kRowBuf entries, sorted, keep the stored prefix valid atom indices)
+                const int m = min(cursor, kRowBuf);
+                const int P = next_pow2(m > 0 ? m : 1);
+                for (int k = m + lane; k < P; k += 32) buf[k] = INT_MAX;
                 __syncwarp();
                 warp_bitonic_sort(buf, P, lane);
                 int32_t* dst = DIRECT ? gdst : a.out + r * (int64_t)kRowCap;
-                const int lim = DIRECT ? cursor : min(cursor, kRowCap);
+                const int lim = DIRECT ? cursor : min(m, kRowCap);
                 for (int k = lane; k < lim; k += 32) dst[k] = buf[k];
-            } else if (DIRECT && lane == 0) {   // very long row: insertion sort in place
+            } else if (lane == 0) {   // DIRECT, very long row: insertion sort in place
                 for (int x = 1; x < cursor; x++) {
                     int v = gdst[x], y = x - 1;
                     while (y >= 0 && gdst[y] > v) {
@@ -973,7 +980,7 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_fallback(ListArgs a) {
             }
             __syncwarp();
             if (lane == 0 && !DIRECT) {
-                a.npart[r] = cursor;
+                a.npart[r] = (a.clamp && cursor > kRowCap) ? kRowCap : cursor;
                 if (cursor > kRowCap) atomicOr(&a.n_overflow[1], 1);
             }
         }
@@ -1240,6 +1247,7 @@ static ListArgs list_args(const double* q, const CellGrid& cg, double rs, int ha
     a.out = out;
     a.n_overflow = (int32_t*)(ws + W.off_over);
     a.overflow_cells = a.n_overflow + 2;
+    a.clamp = 0;
     return a;
 }
 
@@ -1252,8 +1260,14 @@ constexpr size_t kListSmem = (size_t)kMaxCand * 8 + (size_t)(kMaxCand + 32) * (3
 constexpr size_t kListSmemV4 = (size_t)8 * (kMaxCand + 64) * 2 + (size_t)(kMaxCand + 32) * (16 + 1);
 
 static cudaError_t set_list_attrs() {
-    static bool attr = false;
-    if (!attr) {
+    // cudaFuncSetAttribute is per device: one flag per device ordinal (set once, thread-safe)
+    constexpr int kMaxDevices = 64;
+    static std::atomic<bool> done[kMaxDevices];
+    int dev = 0;
+    cudaError_t ed = cudaGetDevice(&dev);
+    if (ed != cudaSuccess) return ed;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    if (!done[dev].load(std::memory_order_acquire)) {
         void (*fns[4])(ListArgs) = {k_list_v2<0, 0>, k_list_v2<0, 1>, k_list_v2<1, 0>, k_list_v2<1, 1>};
         for (auto f : fns) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
@@ -1264,7 +1278,7 @@ static cudaError_t set_list_attrs() {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmemV4);
             if (e != cudaSuccess) return e;
         }
-        attr = true;
+        done[dev].store(true, std::memory_order_release);   // idempotent: a race sets the same attributes twice
     }
     return cudaSuccess;
 }
@@ -1291,6 +1305,7 @@ cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, in
     if (e != cudaSuccess) return e;
     ListArgs a = list_args(q, cg, rs, half, row_begin, row_end, npart, nullptr,
                            out ? out : (int32_t*)(ws + W.off_scratch), ws, W);
+    a.clamp = out != nullptr;   // the caller's padded list: counts clamped to the stride
     e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     launch_list_kernels<0>(a, cg, half, s);

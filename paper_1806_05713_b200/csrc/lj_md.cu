@@ -203,7 +203,8 @@ __global__ void k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p,
 #pragma unroll
                 for (int c = 0; c < 3; c++) d[c] = d[c] > halfL ? d[c] - L : (d[c] < -halfL ? d[c] + L : d[c]);
             }
-            double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+            // the oracle's r^2 (reading O3, no FMA): the same pairs inside r_c
+            double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
             if (r2 < rc2) {
                 double inv6 = 1.0 / (r2 * r2 * r2);
                 pe += w * (4.0 * (inv6 * inv6 - inv6) - vc);

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "liblj.so")
 
 LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 LJ_LIST_PADDED, LJ_LIST_DEFERRED, LJ_PADDED_ROW_STRIDE = 1, 2, 196   # include/liblj.h
+LJ_LANES_IDXV = 1 << 16   # include/liblj.h: index vector loads (lanes_per_row = G | V << 8 | LJ_LANES_IDXV)
 LAYOUTS = {"aos4": 0, "soa": 1, "aos3": 2, "aos8": 3}                    # LJ_LAYOUT_*
 RECIPROCALS = {"newton3": 0, "newton2": 1, "approx": 2, "ieee": 3}       # LJ_RCP_*
 
@@ -26,7 +27,8 @@ RECIPROCALS = {"newton3": 0, "newton2": 1, "approx": 2, "ieee": 3}       # LJ_RC
 EXPORTS = (
     "lj_pack_aos4", "lj_unpack_aos4", "lj_build_list_workspace", "lj_build_list", "lj_build_list_ex", "lj_rebuild",
     "lj_cell_order",
-    "lj_permute_rows", "lj_force_step", "lj_force_step_ex", "lj_force_step_variant", "lj_gather_probe",
+    "lj_permute_rows", "lj_force_step", "lj_default_lanes", "lj_force_step_ex", "lj_force_step_variant",
+    "lj_gather_probe",
     "lj_list_cell_starts", "lj_force_step_half_cells",
     "lj_md_graph_create", "lj_md_graph_launch", "lj_md_graph_force_ms", "lj_md_graph_kernels", "lj_md_graph_destroy",
     "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
@@ -95,6 +97,7 @@ def load() -> ctypes.CDLL:
         "lj_cell_order": (st, [vp, i64, Geom, vp, vp, sz, vp]),
         "lj_permute_rows": (st, [vp, vp, vp, i64, vp]),
         "lj_force_step": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, vp]),
+        "lj_default_lanes": (i32, [i64, i32]),
         "lj_force_step_ex": (st, [vp, vp, i64, Geom, d, i32, i64, i64, vp, vp, vp, i32, i32, vp, vp]),
         "lj_force_step_variant": (st, [i32, i32, vp, vp, i64, Geom, d, i64, i64, vp, vp, vp, i32, vp, vp]),
         "lj_gather_probe": (st, [vp, i64, i64, i64, vp, vp, vp, i32, vp, vp]),
@@ -242,6 +245,17 @@ class ListBuilder:
         self.status = torch.zeros(2, dtype=torch.int64, pin_memory=True) if self.deferred else None
         self._unresolved = None
 
+    def enable_deferred(self) -> None:
+        """Switch a padded builder to LJ_LIST_DEFERRED builds (no host round trip per build)."""
+        if self.padded and not self.deferred:
+            self.deferred = True
+            self.status = torch.zeros(2, dtype=torch.int64, pin_memory=True)
+
+    def max_row_length(self) -> int:
+        """Longest row of the last (resolved) build -- a host synchronisation."""
+        rows = self.row_end - self.row_begin
+        return int(self.npart[:rows].max().item()) if rows > 0 else 0
+
     def _flags(self):
         return (LJ_LIST_PADDED if self.padded else 0) | (LJ_LIST_DEFERRED if self.deferred and self.padded else 0)
 
@@ -354,6 +368,11 @@ def permute_rows(x: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
 
 def _list_args(lst: CSRList):
     return (lst.row_begin, lst.row_end, _ptr(lst.number_of_partners), _ptr(lst.pointer), _ptr(lst.sorted_list))
+
+
+def default_lanes(rows: int, half: bool) -> int:
+    """lj_default_lanes: the lanes_per_row lj_force_step uses for this many rows."""
+    return int(load().lj_default_lanes(int(rows), int(half)))
 
 
 def force_step(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRList, lanes_per_row: int = 0,

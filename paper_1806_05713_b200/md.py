@@ -28,7 +28,6 @@ which has no fallback: it raises if liblj.so or the GPU is missing.
 from __future__ import annotations
 
 import dataclasses
-import math
 import os
 
 import torch
@@ -49,13 +48,29 @@ class LibBackend:
         lj.load()
         self.device = torch.device(device)
         self.n, self.g = n, g
-        # deferred (no host round trip per rebuild) only where no row can come near the
-        # padded stride: expected full-list row length rho 4/3 pi rs^3 with 30 % margin
-        rows_expected = n / g.L ** 3 * 4.0 / 3.0 * math.pi * g.rs ** 3 if g.L > 0 else float("inf")
-        deferred = deferred and 1.3 * rows_expected < lj.LJ_PADDED_ROW_STRIDE
+        # Deferred builds (no host round trip per rebuild) are switched on after the first,
+        # synchronous build, and only if its longest row leaves ROW_MARGIN entries below the
+        # padded stride.  A later row over the stride is still safe: the builder stores
+        # min(count, stride) and raises the overflow flag, which resolve() / StepGraph.finish()
+        # turn into LJ_ERR_UNSUPPORTED.
+        self._want_deferred = bool(deferred)
         self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device, padded=True,
-                                      deferred=deferred)
+                                      deferred=False)
         self.perm = None   # scratch of the re-sorting rebuild (allocated on first use)
+
+    ROW_MARGIN = 24
+
+    def headroom_ok(self) -> bool:
+        """The last build's longest row is at least ROW_MARGIN below the padded stride."""
+        return self.builder.padded and \
+            self.builder.max_row_length() + self.ROW_MARGIN <= lj.LJ_PADDED_ROW_STRIDE
+
+    def _after_build(self, lst):
+        if self._want_deferred and not self.builder.deferred:
+            self._want_deferred = False   # decided once, on the first synchronous build
+            if self.headroom_ok():
+                self.builder.enable_deferred()
+        return lst
 
     def resolve(self, lst):
         """Finish a deferred build (call after a synchronisation)."""
@@ -69,13 +84,13 @@ class LibBackend:
         return torch.empty((n, 4), dtype=torch.float64, device=self.device)
 
     def build(self, q):
-        return self.builder.build(q)
+        return self._after_build(self.builder.build(q))
 
     def rebuild(self, q, p, q_out, p_out, q_ref):
         """Fused wrap + cell-order permutation + list build (lj_rebuild, one cell pass)."""
         if self.perm is None:
             self.perm = torch.empty(self.n, dtype=torch.int64, device=self.device)
-        return self.builder.rebuild(q, p, q_out, p_out, q_ref, self.perm)
+        return self._after_build(self.builder.rebuild(q, p, q_out, p_out, q_ref, self.perm))
 
     def cell_order(self, q):
         """perm[new] = old (stable sort by cell id), using the builder's workspace."""
@@ -150,6 +165,9 @@ class StepGraph:
         self.sim, self.g, self.status = sim, g, status
         self.energy_every, self._energies = energy_every, energies
         self._seen = 0
+        # the graph holds the device pointers of these buffers (ADVICE r01): an eager step
+        # that swaps sim.q / sim.p (a re-sorting rebuild) invalidates it
+        self._q, self._p = sim.q, sim.p
 
     def energies(self):
         """[(step, KE, PE)] of the last completed launch (energy_every > 0; one rank: no reduction)."""
@@ -159,6 +177,9 @@ class StepGraph:
         return [(k * self.energy_every, ke, pe) for k, (ke, pe) in enumerate(e)]
 
     def launch(self):
+        if self.sim.q is not self._q or self.sim.p is not self._p:
+            raise RuntimeError("StepGraph: the driver's q/p buffers changed since the graph was captured "
+                               "(an eager step re-sorted the atoms); create a new graph with sim.graph()")
         self.g.launch()
 
     def finish(self):
@@ -514,6 +535,11 @@ class LeapfrogMD:
         torch.cuda.current_stream().synchronize()
         self.sync_positions()
         self._resolve()
+        if hasattr(self.be, "headroom_ok") and not self.be.headroom_ok():
+            # rebuilds inside the graph write the padded layout; rows this close to the stride
+            # could overflow it (the graph would then stop with LJ_ERR_UNSUPPORTED at finish())
+            raise lj.LJError(lj.LJ_ERR_UNSUPPORTED, "graph: list rows within %d entries of the padded stride; "
+                             "use eager steps" % self.be.ROW_MARGIN)
         if getattr(self.be, "perm", None) is None:
             self.be.perm = torch.empty(self.n, dtype=torch.int64, device=self.q.device)
         status = torch.zeros(4, dtype=torch.int64, device=self.q.device)

@@ -182,7 +182,9 @@ def oracle_force(w, p0, half):
 
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 @pytest.mark.parametrize("half", [True, False])
-@pytest.mark.parametrize("lanes", [0, 1, 4, 8, 16, 32, 4 | 768, 4 | 1024, 16 | 1024])
+@pytest.mark.parametrize("lanes", [0, 1, 4, 8, 16, 32, 4 | 768, 4 | 1024, 16 | 1024,
+                                   2 | 512 | 65536, 4 | 512 | 65536, 4 | 1024 | 65536, 8 | 1024 | 65536,
+                                   1 | 1024 | 65536])
 def test_force_parity(lj, dev, systems, cfg, half, lanes):
     w = systems[cfg]
     rng = np.random.default_rng(cfg)
@@ -698,3 +700,45 @@ def test_deferred_padded_build(lj, dev, systems):
     torch.cuda.synchronize()
     with pytest.raises(lj.LJError):
         bd.resolve()
+
+
+def test_overflowed_padded_list_stays_in_bounds(lj, dev):
+    """a padded row over the stride stores min(count, stride) in
+    number_of_partners, so a force step that runs before the overflow is
+    noticed (deferred build, graph rebuild) reads inside the list; the overflow
+    is still reported (resolve() / the graph status)."""
+    S = lj.LJ_PADDED_ROW_STRIDE
+    qg = to_dev(lj_inputs.random_gas(5000, 9.9, 4), dev)
+    g = lj.geom(9.9, 3.0, 3.3)
+    bd = lj.ListBuilder(5000, g, False, device=dev, padded=True, deferred=True)
+    lst = bd.build(qg)
+    p = to_dev(np.zeros((5000, 3)), dev)
+    lj.force_step(qg, p, g, 0.0, lst)             # before resolve(): must not fault
+    torch.cuda.synchronize()
+    assert int(lst.number_of_partners.max().item()) == S
+    with pytest.raises(lj.LJError):
+        bd.resolve()
+    # graph rebuild: a rho = 1 gas whose first build fits, then a dense cluster appears
+    n, L = 8000, 20.0
+    q0 = lj_inputs.random_gas(n, L, 9)
+    gg = lj.geom(L, 3.0, 3.3)
+    q = to_dev(q0, dev)
+    pm = to_dev(np.zeros((n, 3)), dev)
+    b = lj.ListBuilder(n, gg, False, device=dev, padded=True)
+    b.build(q)
+    assert b.padded
+    q2 = q0.copy()
+    q2[:400] = 10.0 + np.random.default_rng(1).uniform(-1.5, 1.5, (400, 3))   # ~28 atoms per unit volume
+    q.copy_(to_dev(q2, dev))
+    q_ref = q.clone()
+    q_ref[:, 0] += 1.0                            # displacement 1 > margin/2: the graph rebuilds at once
+    disp = torch.zeros(1, dtype=torch.float64, device=dev)
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    perm = torch.empty(n, dtype=torch.int64, device=dev)
+    gr = lj.MDGraph(q, pm, None, None, q_ref, perm, gg, 0.0, b, disp, None, status, False, 3)
+    gr.launch()
+    torch.cuda.synchronize()                      # no fault: the steps after the rebuild stay in bounds
+    st = status.tolist()
+    assert st[0] >= 1 and st[1] == 1              # rebuilt, overflow flagged
+    assert int(b.npart.max().item()) == S
+    gr.close()

@@ -183,3 +183,14 @@ def test_integrate_and_displacement():
     # tiny negative rounds to L in x - L*floor(x/L): guarded back to 0 (C-3)
     w = oracle.wrap(np.array([[-1e-18, 0.0, 0.0]]), 10.0)
     assert 0.0 <= w[0, 0] < 10.0
+
+
+def test_all_core_timing_build_is_bit_identical(cfg1):
+    """The OpenMP timing leg (liblj_oracle_omp.so, bench.py cpu_baseline all-core run)
+    splits full-list rows over threads; each row's arithmetic is unchanged."""
+    w, half, full, p0, S = cfg1
+    ref = oracle.force_step(w.q, p0, w.L, w.rc, w.dt, full)
+    p = np.ascontiguousarray(p0.copy())
+    q = np.ascontiguousarray(w.q)
+    oracle.force_step_full_rows_parallel(q, p, w.L, w.rc, w.dt, full, threads=4)
+    assert np.array_equal(p, ref)

@@ -28,8 +28,11 @@ p = lj.pack_aos4(torch.from_numpy(w.p).cuda())
 q = lj.permute_rows(q0, lj.cell_order(q0, g))
 lst = lj.ListBuilder(w.n, g, False, device="cuda", padded=True).build(q)
 sink = torch.zeros(1, dtype=torch.float64, device="cuda")
-for G, U in ((4, 2), (4, 3), (8, 2), (8, 3), (16, 2), (16, 3), (16, 4), (32, 2), (32, 4)):
-    lanes = G | (U << 8)
+IDXV = lj.LJ_LANES_IDXV
+variants = [(G, U, 0) for G, U in ((2, 2), (2, 3), (4, 2), (4, 3), (4, 4), (8, 2), (8, 3), (8, 4), (16, 2), (16, 3))]
+variants += [(G, V, IDXV) for G in (2, 4, 8) for V in (2, 4)] + [(16, 4, IDXV)]
+for G, U, X in variants:
+    lanes = G | (U << 8) | X
     try:
         f = timeit(lambda: lj.force_step(q, p, g, w.dt, lst, lanes_per_row=lanes))
     except lj.LJError as e:
@@ -38,4 +41,5 @@ for G, U in ((4, 2), (4, 3), (8, 2), (8, 3), (16, 2), (16, 3), (16, 4), (32, 2),
         pr = timeit(lambda: lj.gather_probe(q, lst, lanes, sink))
     except lj.LJError:
         pr = None
-    print(json.dumps({"cfg": cfg, "G": G, "U": U, "force_ms": f and round(f, 4), "probe_ms": pr and round(pr, 4)}))
+    print(json.dumps({"cfg": cfg, "G": G, "U": U, "idxv": bool(X), "force_ms": f and round(f, 4),
+                      "probe_ms": pr and round(pr, 4), "entries": lst.n_entries}), flush=True)

@@ -190,3 +190,91 @@ int mb_stream(const void* a, int64_t bytes, int* out, void* stream) {
     return (int)cudaGetLastError();
 }
 }
+
+// ---- B-15 (round 2): uniform random 32-B gathers and fp64 RED throughput ----------
+// Random gathers: record index = hash(thread, k) mod n (integer ALU, no index
+// stream), 8 independent gathers in flight per thread; bytes = 32 per gather.
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+
+__global__ void k_random_gather(const rec4* __restrict__ q, uint32_t n, int iters, double* out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    double s = 0;
+    for (int it = 0; it < iters; it++) {
+        rec4 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) a[u] = ldrec(q + (hash32(t * 131u + (uint32_t)(it * 8 + u) * 0x9e3779b9u) % n));
+#pragma unroll
+        for (int u = 0; u < 8; u++) s += a[u].x + a[u].y + a[u].z;
+    }
+    if (s == 12345.678) out[0] = s;
+}
+
+// fp64 RED throughput: each thread adds to the x, y, z of random records (the half
+// list's 24-B p_j read-modify-write per entry: 3 RED.E.ADD.F64), 4 records per
+// iteration.
+__global__ void k_random_red(double* p, uint32_t n, int iters) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t j = hash32(t * 977u + (uint32_t)(it * 4 + u) * 0x9e3779b9u) % n;
+            atomicAdd(p + 4 * (size_t)j + 0, 1e-30);
+            atomicAdd(p + 4 * (size_t)j + 1, 1e-30);
+            atomicAdd(p + 4 * (size_t)j + 2, 1e-30);
+        }
+    }
+}
+
+// The half list's RED pattern on its own: for every entry of every row, 3 REDs
+// to p_j (G lanes per row, as k_force), and 3 REDs to p_i per row -- no gathers,
+// no arithmetic (the atomics floor of the half-list kernel).
+template <int G>
+__global__ void k_half_red_replay(double* p, int64_t rows, const int32_t* __restrict__ npart,
+                                  const int64_t* __restrict__ ptr, const int32_t* __restrict__ list) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    if (r >= rows) return;
+    const int32_t* l = list + ptr[r];
+    const int n = npart[r];
+    for (int k = g; k < n; k += G) {
+        const int j = __ldg(l + k);
+        atomicAdd(p + 4 * (size_t)j + 0, 1e-30);
+        atomicAdd(p + 4 * (size_t)j + 1, 1e-30);
+        atomicAdd(p + 4 * (size_t)j + 2, 1e-30);
+    }
+    if (g == 0) {
+        atomicAdd(p + 4 * r + 0, 1e-30);
+        atomicAdd(p + 4 * r + 1, 1e-30);
+        atomicAdd(p + 4 * r + 2, 1e-30);
+    }
+}
+
+extern "C" {
+int mb_random_gather(const double* q, int64_t n, int blocks, int threads, int iters, double* out, void* stream) {
+    k_random_gather<<<blocks, threads, 0, (cudaStream_t)stream>>>((const rec4*)q, (uint32_t)n, iters, out);
+    return (int)cudaGetLastError();
+}
+int mb_random_red(double* p, int64_t n, int blocks, int threads, int iters, void* stream) {
+    k_random_red<<<blocks, threads, 0, (cudaStream_t)stream>>>(p, (uint32_t)n, iters);
+    return (int)cudaGetLastError();
+}
+int mb_half_red_replay(double* p, int64_t rows, const int32_t* npart, const int64_t* ptr, const int32_t* list, int G,
+                       void* stream) {
+    const unsigned grid = (unsigned)((rows * G + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (G) {
+        case 4: k_half_red_replay<4><<<grid, 256, 0, s>>>(p, rows, npart, ptr, list); break;
+        case 8: k_half_red_replay<8><<<grid, 256, 0, s>>>(p, rows, npart, ptr, list); break;
+        default: return -1;
+    }
+    return (int)cudaGetLastError();
+}
+}
