@@ -224,6 +224,33 @@ def run_reference(args):
 
 # ---- our arm ----------------------------------------------------------------------
 
+# the five fastest gather-replay variants of the B-15 sweep (profiles/r02_b15.json, config 4)
+PROBE_VARIANTS = [4 | 3 << 8, 8 | 2 << 8, 8 | 3 << 8, 16 | 2 << 8, 16 | 3 << 8]
+
+
+def lanes_str(lanes):
+    s = f"G{lanes & 0xff}/U{(lanes >> 8) & 0xff}"
+    return s + ("/idxv" if lanes & (1 << 16) else "")
+
+
+def load_b15():
+    p = os.path.join(ROOT, "profiles", "r02_b15.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
+def timed_ms(fn, stream):
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    fn()
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b)
+
+
 def spawn_ranks(n):
     """`bench.py --gpus N` launched as a single process: re-execute it as N ranks, one
     per GPU, under torch.distributed.run (the driver's own launch line).  Fails loudly
@@ -355,12 +382,21 @@ def main():
     # MD configs on one rank: the whole step -- kick, drift + displacement, the rebuild
     # decision and the conditional rebuild -- as one CUDA graph over the K timed steps
     # (lj_md_graph, device-side decision: no host round trip per step or rebuild)
+    # (P > 1, or P = 1 with LJ_FORCE_COLLECTIVES=1: graph_collective -- the NCCL all-gather captured
+    # in the same graph, the decision from the displacements the all-gather carries in the q pads)
     md_graph = None
     graph_note = ""
-    if not force_only and not args.no_graph and not sim.collective:
+    if not force_only and not args.no_graph:
         try:
-            md_graph = sim.graph(args.steps, energy_every=every)
-        except lj.LJError as ex:   # e.g. a driver without conditional graph nodes: eager GPU steps
+            if sim.collective:
+                if every > 0:
+                    raise ValueError("energy samples at P > 1 run eagerly")
+                if args.exchange != "allgather":
+                    raise ValueError(f"--exchange {args.exchange} runs eagerly")
+                md_graph = sim.graph_collective(args.steps)
+            else:
+                md_graph = sim.graph(args.steps, energy_every=every)
+        except (lj.LJError, ValueError) as ex:   # eager GPU steps instead
             graph_note = f" (graph unavailable: {ex})"
     lj_graph_launches = [0]
     sim.interactions()   # reset counter
@@ -403,63 +439,88 @@ def main():
     value = pairs / (ms_max * 1e-3)
     rebuilds = sim.stats.rebuilds - reb0
     force_ms = f_ms_graph if md_graph is not None else [a.elapsed_time(b) for a, b in f_ev]
+    force_note = "CUDA-event nodes around every timed step's force kernel (inside the timed region)"
+    if not force_ms:
+        # graph_collective has no per-step event nodes: time the same kernel on the final list,
+        # on a scratch copy of p, right after the timed region
+        pc = sim.p.clone()
+        force_ms = [timed_ms(lambda: be.force(sim.q, pc, w.dt, sim.lst), stream) for _ in range(10)]
+        force_note = "10 launches of the same kernel on the final list after the timed region"
+        del pc
     force_avg = sum(force_ms) / len(force_ms)
     entries_per_launch = sim.lst.n_entries       # own rows (last list)
 
     # ---- roofline of the dominant kernel (the force step) ----
-    # BASELINE.json north_star: "the slower of its partner-gather bytes at achieved
-    # L2/HBM bandwidth and its FP64 flops at peak".  The gather floor is measured
-    # live: lj_gather_probe replays the same list with the same lanes (index loads
-    # + 256-bit record gathers, no arithmetic); the FP64 floor is the paper's 22
-    # flop per entry at the derived FP64 peak.
+    # The full-list force kernel is bound by its partner gathers: every entry is one random
+    # 32-B record load served by L1/L2 (the L1TEX data pipe runs at ~93 % of its wavefront peak,
+    # ncu; FP64 at ~40 %).  Its floor is the force kernel's own access pattern without the
+    # arithmetic -- lj_gather_probe on this list -- timed live here for the five fastest
+    # lanes/unroll variants of the B-15 sweep (profiles/r02_b15.json); the fastest is the
+    # "best same-list replay" (not the kernel's own G/U).  achieved / peak are the
+    # algorithmic bytes of a launch (36 B per entry + 108 B per row) over the
+    # force kernel's and the best replay's durations, so frac = best replay / force.
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     peak_tflops = N_SM * FP64_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
     E = entries_per_launch
     rows_own = re_ - rb
-    probe_ms = None
-    if not force_only or not half:
-        sink = torch.zeros(1, dtype=torch.float64, device=dev)
-        for _ in range(3):
-            lj.gather_probe(sim.q, sim.lst, 0, sink)
-        pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        pa.record(stream)
-        for _ in range(10):
-            lj.gather_probe(sim.q, sim.lst, 0, sink)
-        pb.record(stream)
-        torch.cuda.synchronize()
-        probe_ms = pa.elapsed_time(pb) / 10
     gather_bytes = BYTES_PER_ENTRY * E + BYTES_PER_ROW * rows_own   # SURVEY §8(d) algorithmic bytes per launch
     fp64_ms = FLOP_PER_ENTRY * E / (peak_tflops * 1e12) * 1e3
-    traffic = None
+    b15 = load_b15()
     tp = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
+    tj = {}
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
-        traffic = tj.get("dram_bytes_per_launch")
-        l1_pct = tj.get("l1tex_lsu_wavefront_pct_of_peak")
-    else:
-        l1_pct = None
+    traffic = tj.get("dram_bytes_per_launch")
     roof = None
-    if probe_ms is not None:
-        floor_ms = max(probe_ms, fp64_ms)
-        roof = {"bound": "hbm" if probe_ms >= fp64_ms else "alu",
+    if not half:
+        sink = torch.zeros(1, dtype=torch.float64, device=dev)
+        probes = {}
+        for lanes in PROBE_VARIANTS + [lj.default_lanes(rows_own, False)]:
+            lj.gather_probe(sim.q, sim.lst, lanes, sink)
+            probes[lanes] = min(timed_ms(lambda: lj.gather_probe(sim.q, sim.lst, lanes, sink), stream)
+                                for _ in range(10))
+        best_lanes = min(probes, key=probes.get)
+        best_ms = probes[best_lanes]
+        dram = None
+        if traffic:
+            dram = {"bytes_per_launch": traffic, "achieved_gbs": traffic / (force_avg * 1e-3) / 1e9,
+                    "peak_gbs": pk.get("hbm_gbs"), "peak_kind": pk_kind,
+                    "frac": traffic / (force_avg * 1e-3) / 1e9 / pk.get("hbm_gbs", 6448.4),
+                    "source": f"profiles/traffic_config{args.config}.json (ncu --set full of this kernel)"}
+        roof = {"bound": "l1_data_pipe",
                 "achieved": gather_bytes / (force_avg * 1e-3) / 1e9,
-                "peak": gather_bytes / (floor_ms * 1e-3) / 1e9,
-                "unit": "GB/s", "frac": floor_ms / force_avg, "traffic": traffic,
-                "kernel": "k_force (full list, 4 lanes per row, 3 gathers in flight per lane)",
-                "definition": "BASELINE.json north_star: slower of partner-gather bytes at achieved L2/HBM "
-                              "bandwidth (lj_gather_probe, same list and lanes, measured live) and FP64 at peak",
+                "peak": gather_bytes / (best_ms * 1e-3) / 1e9,
+                "unit": "GB/s", "frac": best_ms / force_avg, "traffic": traffic,
+                "peak_kind": "measured live: best same-list gather replay (lj_gather_probe: index loads + one "
+                             "256-bit record gather per entry, no arithmetic) over lanes variants "
+                             + ", ".join(lanes_str(x) for x in probes),
+                "kernel": f"k_force (full list, lanes_per_row {lanes_str(lj.default_lanes(rows_own, False))})",
+                "force_ms": force_avg, "force_ms_source": force_note,
+                "best_replay": {"lanes_per_row": lanes_str(best_lanes), "ms": best_ms},
+                "replay_ms": {lanes_str(k): v for k, v in probes.items()},
                 "bytes_per_entry": BYTES_PER_ENTRY, "bytes_per_row": BYTES_PER_ROW, "entries_per_launch": E,
-                "gather_floor_ms": probe_ms, "fp64_floor_ms": fp64_ms,
-                "alu_view": {"achieved_tflops": FLOP_PER_ENTRY * E / (force_avg * 1e-3) / 1e12,
-                             "peak_tflops": peak_tflops, "frac": fp64_ms / force_avg, "flop_per_entry": FLOP_PER_ENTRY,
-                             "peak_kind": f"derived: {N_SM} SM x {FP64_LANES_PER_SM} FP64 lanes x 2 x {sm_mhz:.0f} MHz"},
-                "hbm_peak_view": {"achieved_gbs": gather_bytes / (force_avg * 1e-3) / 1e9,
-                                  "peak_gbs": pk.get("hbm_gbs"), "peak_kind": pk_kind,
-                                  "frac": gather_bytes / (force_avg * 1e-3) / 1e9 / pk.get("hbm_gbs", 6448.4),
-                                  "note": "> 1: the gathers are served by L1/L2 (DRAM traffic per launch = traffic)"},
-                "l1_view": {"lsu_data_pipe_wavefronts_pct_of_peak": l1_pct,
-                            "source": f"profiles/traffic_config{args.config}.json (ncu --set full of this kernel)"}}
+                "l1_data_pipe_pct_of_peak": tj.get("l1tex_lsu_wavefront_pct_of_peak"),
+                "dram": dram,
+                "fp64": {"achieved_tflops": FLOP_PER_ENTRY * E / (force_avg * 1e-3) / 1e12,
+                         "peak_tflops": peak_tflops, "frac": fp64_ms / force_avg, "flop_per_entry": FLOP_PER_ENTRY,
+                         "peak_kind": f"derived: {N_SM} SM x {FP64_LANES_PER_SM} FP64 lanes x 2 x {sm_mhz:.0f} MHz"
+                                      + (f"; measured DFMA {b15['fp64_fma']['TFLOP_s']:.1f} TFLOP/s" if b15 else "")},
+                "random_gather_context": (b15 or {}).get("random_gather")}
+    else:
+        # half list (Alg. 3): 3 fp64 REDs per entry (the 24-B p_j RMW) + 3 per row;
+        # the denominator is the measured RED throughput (profiles/r02_b15.json random_red)
+        reds = 3.0 * (E + rows_own)
+        red_peak = None
+        if b15:
+            red_peak = max(r["G_red_f64_per_s"] for r in b15["random_red"])
+        roof = {"bound": "red", "achieved": reds / (force_avg * 1e-3) / 1e9, "peak": red_peak,
+                "unit": "G RED.F64/s", "frac": (reds / (force_avg * 1e-3) / 1e9 / red_peak) if red_peak else None,
+                "traffic": traffic, "kernel": f"k_force (half list, lanes_per_row {lanes_str(lj.default_lanes(rows_own, True))})",
+                "peak_kind": "measured: fp64 RED throughput to random records (tools/roofline_b15.py, "
+                             "profiles/r02_b15.json)",
+                "force_ms": force_avg, "reds_per_launch": reds,
+                "half_list_red_replay": (b15 or {}).get("half_red_replay")}
 
     # ---- repeats of the timed steps (SURVEY §8(d) timing protocol: min and median) ----
     repeats = None
@@ -589,7 +650,9 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config{args.config}", "n_atoms": w.n, "list": "half" if half else "full",
-                       "order": order + (" (re-sorted at every rebuild)" if order == "cell" and not force_only else ""),
+                       "order": order + ((" (sorted once, then fixed row ownership)" if sim.collective and
+                                          md_graph is not None else " (re-sorted at every rebuild)")
+                                         if order == "cell" and not force_only else ""),
                        "dt": w.dt, "rc": w.rc, "rs": w.rs, "parallelism": f"rows/{world}",
                        "exchange": (("fused integrate + NVLink push" if sim.push else "halo" if sim.halo else "all-gather")
                                     + (" (async, overlapped with the interior rows' force)" if sim.overlap else "")
@@ -601,7 +664,10 @@ def main():
             "cuda_graph": (graph is not None or md_graph is not None),
             "interactions_counted": ("once (q fixed in the force-only configs), x steps" if counted_once is not None
                                      else "live, every timed step (kernel counter)"),
-            "step_control": ("device (lj_md_graph: conditional rebuild node, one graph launch for the timed steps)"
+            "step_control": (("device (graph_collective: NCCL all-gather + conditional rebuild node captured in one "
+                              "graph for the timed steps; decision from the displacements carried in the q pads)"
+                              if sim.collective else
+                              "device (lj_md_graph: conditional rebuild node, one graph launch for the timed steps)")
                              if md_graph is not None else "host" + graph_note),
             "roofline": roof,
             "repeats": repeats,

@@ -363,6 +363,46 @@ lj_status lj_md_graph_force_ms(const lj_md_graph *gr, float *ms, int n);
 lj_status lj_md_graph_kernels(const lj_md_graph *gr, long long *steps_total, long long *per_rebuild);
 lj_status lj_md_graph_destroy(lj_md_graph *gr);
 
+/* ---- the multi-rank step under the caller's stream capture (P > 1; SURVEY
+ * §8(f) NEXT-1 "capture the whole step, NCCL included, in a CUDA graph") ---- */
+
+/* Buffers of one rank's bookkeeping rebuild (fixed row ownership, no re-sort:
+ * SURVEY §8(e)); device memory owned by the caller. */
+typedef struct {
+    double *q;                /* n records: replicated positions (complete after the position exchange) */
+    double *q_ref;            /* n records: bookkeeping reference (written by every rebuild) */
+    int64_t n;
+    lj_geom g;
+    int64_t row_begin, row_end;   /* own rows */
+    int32_t *number_of_partners;  /* own rows' padded list (LJ_LIST_PADDED), current before the first launch */
+    int64_t *pointer;
+    int32_t *sorted_list;
+    int64_t capacity;         /* >= (row_end - row_begin) * LJ_PADDED_ROW_STRIDE */
+    void *workspace;          /* lj_build_list_workspace(n, g) bytes */
+    size_t workspace_bytes;
+    const double *disp;       /* the decision reads max_k disp[k * disp_stride], k < disp_count: e.g. the */
+    int disp_count;           /* pads of every rank's first q record after the all-gather (see */
+    int64_t disp_stride;      /* lj_publish_scalar), or one all-reduced double (count 1, stride 0) */
+    int64_t *status;          /* 4 int64, as lj_md_graph_desc.status */
+} lj_md_rebuild_desc;
+
+/* Called while `stream` is being captured into a CUDA graph (cudaStreamBeginCapture
+ * in relaxed mode, e.g. inside torch.cuda.graph holding the step's NCCL
+ * collectives): appends to the capture a one-thread kernel that takes the
+ * bookkeeping decision (rebuild iff 2 max_k disp[k*stride] >= rs - rc, reading
+ * C-16) and an IF node whose body wraps all n records of q
+ * (q_ref = the wrapped q, as lj_wrap) and rebuilds the own rows' padded list
+ * (as lj_build_list_ex, status to d->status as lj_md_graph).  Work captured
+ * afterwards on `stream` depends on the IF node.  *kernels_per_rebuild (if not
+ * NULL) = kernels the body launches.  LJ_ERR_ARG if `stream` is not capturing. */
+lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc *d, void *stream, long long *kernels_per_rebuild);
+
+/* dst[0] = src[0] (device doubles), stream-ordered: e.g. the rank's maximum
+ * displacement into the pad lane of its first own q record, which the position
+ * all-gather then carries to every rank -- the bookkeeping decision without a
+ * separate all-reduce.  Pads are ignored by every kernel. */
+lj_status lj_publish_scalar(const double *src, double *dst, void *stream);
+
 /* Wrap q into [0,L) (x -= L floor(x/L); x -= L if x >= L) for atoms [0,n) and,
  * if q_ref != NULL, copy the wrapped records to q_ref (the bookkeeping
  * reference of PAPER.md:190-192). */

@@ -662,7 +662,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
         }
         if (e == cudaSuccess) e = launch_integrate_disp(d->q, d->p, d->q_ref, 0, n, d->dt, d->disp, cs);
         if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, gr->graph, 0, cudaGraphCondAssignDefault);
-        if (e == cudaSuccess) e = launch_md_decide(d->disp, d->g.rs - d->g.rc, h, d->status, cs);
+        if (e == cudaSuccess) e = launch_md_decide(d->disp, 1, 0, d->g.rs - d->g.rc, h, d->status, cs);
         const cudaGraphNode_t* deps = nullptr;
         size_t ndeps = 0;
         cudaStreamCaptureStatus cst;
@@ -712,6 +712,80 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
     LJ_G(cudaStreamSynchronize(cs), "md_graph/upload");
 #undef LJ_G
     return done(LJ_OK);
+}
+
+lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long long* kernels_per_rebuild) {
+    if (!d) return fail(LJ_ERR_ARG, "md_capture_rebuild: null descriptor");
+    const int64_t n = d->n;
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(d->g, true));
+    LJ_TRY(check_rows(n, d->row_begin, d->row_end));
+    if (n < 1) return fail(LJ_ERR_ARG, "md_capture_rebuild: n must be >= 1");
+    if (!d->q || !d->q_ref || !d->number_of_partners || !d->pointer || !d->sorted_list || !d->workspace ||
+        !d->disp || !d->status)
+        return fail(LJ_ERR_ARG, "md_capture_rebuild: null pointer");
+    if (!aligned32(d->q) || !aligned32(d->q_ref)) return fail(LJ_ERR_ARG, "md_capture_rebuild: records not 32-byte aligned");
+    if (d->disp_count < 1 || d->disp_count > 4096 || d->disp_stride < 0)
+        return fail(LJ_ERR_ARG, "md_capture_rebuild: need 1 <= disp_count <= 4096, disp_stride >= 0");
+    const int64_t rows = d->row_end - d->row_begin;
+    if (d->capacity < rows * (int64_t)LJ_PADDED_ROW_STRIDE)
+        return fail(LJ_ERR_CAPACITY, "md_capture_rebuild: the padded list needs capacity %lld",
+                    (long long)(rows * (int64_t)LJ_PADDED_ROW_STRIDE));
+    const CellGrid cg = make_grid(d->g);
+    const BuildWorkspace W = build_workspace_layout(n, cg.ncell, n);
+    if (d->workspace_bytes < W.total) return fail(LJ_ERR_ARG, "md_capture_rebuild: workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t graph = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    LJ_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, &graph, &deps, &ndeps), "md_capture_rebuild/info");
+    if (cst != cudaStreamCaptureStatusActive || !graph)
+        return fail(LJ_ERR_ARG, "md_capture_rebuild: the stream is not being captured");
+    cudaGraphConditionalHandle h;
+    LJ_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault), "md_capture_rebuild/handle");
+    LJ_CUDA(launch_md_decide(d->disp, d->disp_count, d->disp_stride, d->g.rs - d->g.rc, h, d->status, s),
+            "md_capture_rebuild/decide");
+    LJ_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, &graph, &deps, &ndeps), "md_capture_rebuild/info");
+    std::vector<cudaGraphNode_t> leaf(deps, deps + ndeps);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    LJ_CUDA(cudaGraphAddNode(&node, graph, leaf.data(), leaf.size(), &cp), "md_capture_rebuild/conditional");
+    // the body: captured on a private stream into the conditional's graph
+    cudaStream_t bs = nullptr;
+    LJ_CUDA(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking), "md_capture_rebuild/stream");
+    cudaError_t e = cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeRelaxed);
+    const long long l0 = g_launches;
+    lj_status st = LJ_OK;
+    if (e == cudaSuccess) {
+        e = launch_wrap(d->q, d->q_ref, n, d->g.L, bs);
+        if (e == cudaSuccess)
+            st = build_list_impl(d->q, n, d->g, 0, d->row_begin, d->row_end, LJ_LIST_PADDED, d->number_of_partners,
+                                 d->pointer, d->sorted_list, d->capacity, d->status + 2, d->workspace,
+                                 d->workspace_bytes, bs, nullptr, d->status);
+        cudaGraph_t tmp;
+        const cudaError_t e2 = cudaStreamEndCapture(bs, &tmp);
+        if (e == cudaSuccess) e = e2;
+    }
+    cudaStreamDestroy(bs);
+    if (st != LJ_OK) return st;
+    LJ_CUDA(e, "md_capture_rebuild/body");
+    if (kernels_per_rebuild) *kernels_per_rebuild = g_launches - l0;
+    // later captured work on `stream` follows the IF node
+    LJ_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies),
+            "md_capture_rebuild/deps");
+    return LJ_OK;
+}
+
+lj_status lj_publish_scalar(const double* src, double* dst, void* stream) {
+    if (!src || !dst) return fail(LJ_ERR_ARG, "publish_scalar: null pointer");
+    LJ_CUDA(launch_copy_scalar(src, dst, (cudaStream_t)stream), "lj_publish_scalar");
+    return LJ_OK;
 }
 
 lj_status lj_md_graph_force_ms(const lj_md_graph* gr, float* ms, int n) {

@@ -39,6 +39,7 @@ struct PairConsts {
     double c48, c24; // 48 dt, 24 dt
     double rc2;      // r_c^2 = rc*rc (the oracle's constant)
     long long rc2_bits;
+    int rc2_hi;      // high word of rc2's IEEE bits
     int hi_halfL;    // high word of L/2 (INT_MAX for open boundaries)
     int hi_L2q;      // high word of (L/2)^2: r^2 below it needs no image (INT_MAX for open boundaries)
 };
@@ -53,19 +54,20 @@ __device__ __forceinline__ double fast_rcp(double x) {
 // The cutoff test on the oracle's r^2 (readings O3/C-4: r2 = (dx*dx + dy*dy) + dz*dz
 // without FMA, interact iff r2 < rc2).  The kernels evaluate r^2 with FMAs
 // (fma(dz, dz, fma(dy, dy, dx*dx))), which differs from the oracle's rounding by
-// at most ~3 ulp; within kCutBand ulp of rc2 the decision is retaken on the
-// oracle's expression (explicit _rn operations), so the set of interacting pairs
-// is the oracle's bit for bit.  The band is hit by ~1e-13 of the entries of the
-// workloads (rare, divergent path).
-constexpr long long kCutBand = 64;
+// at most a few ulp.  The decision is taken on the HIGH words of the IEEE bits
+// (r^2 > 0, so bit order = value order): hi(r2) < hi(rc2) - 1 is inside and
+// hi(r2) > hi(rc2) + 1 outside for either rounding (they are >= 2^32 ulp from
+// rc2); the ~3e-6-relative window in between -- ~5e-6 of the entries of the
+// workloads -- is re-evaluated on the oracle's expression with explicit _rn
+// operations, so the set of interacting pairs is the oracle's bit for bit.
 __device__ __forceinline__ bool inside_cutoff(double r2, double dx, double dy, double dz, const PairConsts& c) {
-    const long long d = __double_as_longlong(r2) - c.rc2_bits;
-    if ((unsigned long long)(d + kCutBand) > (unsigned long long)(2 * kCutBand)) return d < 0;
+    const int dh = __double2hiint(r2) - c.rc2_hi;
+    if ((unsigned)(dh + 1) > 2u) return dh < 0;
     const double r2e = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
     return r2e < c.rc2;
 }
-// The same for U entries at once: the common decision on the bits, the exact
-// re-evaluation in one rarely taken block (keeps the hot loop's registers).
+// The same for U entries at once: the common decision on the high words, the
+// exact re-evaluation in one rarely taken block (keeps the hot loop's registers).
 template <int U>
 __device__ __forceinline__ void inside_cutoff_u(bool (&in)[U], const int (&j)[U], const double (&r2)[U],
                                                 const double (&dx)[U], const double (&dy)[U], const double (&dz)[U],
@@ -73,9 +75,9 @@ __device__ __forceinline__ void inside_cutoff_u(bool (&in)[U], const int (&j)[U]
     bool near = false;
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        const long long d = __double_as_longlong(r2[u]) - c.rc2_bits;
-        in[u] = j[u] >= 0 && d < 0;
-        near |= (unsigned long long)(d + kCutBand) <= (unsigned long long)(2 * kCutBand);
+        const int dh = __double2hiint(r2[u]) - c.rc2_hi;
+        in[u] = j[u] >= 0 && dh < 0;
+        near |= (unsigned)(dh + 1) <= 2u;
     }
     if (__builtin_expect(near, 0)) {
 #pragma unroll
@@ -841,6 +843,7 @@ PairConsts make_consts(const ForceArgs& a) {
     } u;
     u.d = a.rc2;
     c.rc2_bits = u.b;
+    c.rc2_hi = (int)(u.b >> 32);
     c.rc2 = a.rc2;
     if (a.L > 0.0) {
         u.d = 0.5 * a.L;

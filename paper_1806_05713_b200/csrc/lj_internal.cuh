@@ -96,8 +96,9 @@ cudaError_t launch_integrate_push(const double* q_in, double* q_out, const doubl
                                   int64_t begin, int64_t end, double dt, double* out, const lj_push_target* t,
                                   int n_targets, cudaStream_t s);
 cudaError_t launch_wrap(double* q, double* q_ref, int64_t n, double L, cudaStream_t s);
-cudaError_t launch_md_decide(const double* disp, double margin, cudaGraphConditionalHandle h, int64_t* status,
-                             cudaStream_t s);
+cudaError_t launch_md_decide(const double* disp, int count, int64_t stride, double margin,
+                             cudaGraphConditionalHandle h, int64_t* status, cudaStream_t s);
+cudaError_t launch_copy_scalar(const double* src, double* dst, cudaStream_t s);
 cudaError_t launch_build_status(const int64_t* total, const int32_t* row_overflow, int64_t* status, cudaStream_t s);
 cudaError_t launch_max_disp(const double* q, const double* q_ref, int64_t begin, int64_t end, double* out,
                             cudaStream_t s);

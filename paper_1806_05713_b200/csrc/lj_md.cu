@@ -167,9 +167,11 @@ __global__ void k_integrate_push(const rec4* q_in, rec4* q_out, const rec4* __re
 // The bookkeeping decision of the MD step (reading C-16: rebuild when
 // 2 max|q - q_ref| >= r_s - r_c) taken on the device: sets the graph's IF
 // condition and counts rebuilds in status[0].
-__global__ void k_md_decide(const double* __restrict__ disp, double margin, cudaGraphConditionalHandle h,
-                            int64_t* status) {
-    const bool r = 2.0 * disp[0] >= margin;
+__global__ void k_md_decide(const double* __restrict__ disp, int count, int64_t stride, double margin,
+                            cudaGraphConditionalHandle h, int64_t* status) {
+    double m = disp[0];
+    for (int k = 1; k < count; k++) m = fmax(m, disp[k * stride]);
+    const bool r = 2.0 * m >= margin;
     cudaGraphSetConditional(h, r ? 1u : 0u);
     if (r) status[0] += 1;
 }
@@ -182,31 +184,42 @@ __global__ void k_build_status(const int64_t* __restrict__ total, const int32_t*
     if (row_overflow && *row_overflow) status[1] = 1;
 }
 
-// KE over own rows and shifted PE over list entries inside r_c (thread per row).
-__global__ void k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p, int64_t row_begin, int64_t rows,
-                         const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr,
-                         const int32_t* __restrict__ list, double L, double rc2, double vc, int half,
-                         double* out) {
+// KE over own rows and shifted PE (reading O7) over the list entries inside r_c.
+// G = 8 lanes per row (as the force kernel: one 256-bit record gather per
+// entry, coalesced index loads), the cutoff on the oracle's r^2 (no FMA), the
+// minimum image as the oracle's branches; per-lane sums reduced per block.
+constexpr int kEnergyLanes = 8;
+__global__ void __launch_bounds__(kThreads)
+    k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p, int64_t row_begin, int64_t rows,
+             const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
+             double L, double rc2, double vc, int half, double* out) {
+    constexpr int G = kEnergyLanes;
     double ke = 0.0, pe = 0.0;
     const double halfL = 0.5 * L;
     const double w = half ? 1.0 : 0.5;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int g = threadIdx.x % G;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) / G) {
         const int64_t i = row_begin + r;
-        const rec4 qi = q[i], pi = p[i];
-        ke += 0.5 * (pi.x * pi.x + pi.y * pi.y + pi.z * pi.z);
-        const int64_t beg = ptr[r];
+        const rec4 qi = load_rec(q, i);
+        if (g == 0) {
+            const rec4 pi = p[i];
+            ke += 0.5 * __dadd_rn(__dadd_rn(__dmul_rn(pi.x, pi.x), __dmul_rn(pi.y, pi.y)), __dmul_rn(pi.z, pi.z));
+        }
+        const int32_t* __restrict__ l = list + ptr[r];
         const int n = npart[r];
-        for (int k = 0; k < n; k++) {
-            const rec4 qj = load_rec(q, list[beg + k]);
-            double d[3] = {qj.x - qi.x, qj.y - qi.y, qj.z - qi.z};
+        for (int k = g; k < n; k += G) {
+            const rec4 qj = load_rec(q, __ldg(l + k));
+            double dx = qj.x - qi.x, dy = qj.y - qi.y, dz = qj.z - qi.z;
             if (L > 0.0) {
-#pragma unroll
-                for (int c = 0; c < 3; c++) d[c] = d[c] > halfL ? d[c] - L : (d[c] < -halfL ? d[c] + L : d[c]);
+                dx = dx > halfL ? dx - L : (dx < -halfL ? dx + L : dx);
+                dy = dy > halfL ? dy - L : (dy < -halfL ? dy + L : dy);
+                dz = dz > halfL ? dz - L : (dz < -halfL ? dz + L : dz);
             }
             // the oracle's r^2 (reading O3, no FMA): the same pairs inside r_c
-            double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
+            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
             if (r2 < rc2) {
-                double inv6 = 1.0 / (r2 * r2 * r2);
+                const double inv6 = 1.0 / (r2 * r2 * r2);
                 pe += w * (4.0 * (inv6 * inv6 - inv6) - vc);
             }
         }
@@ -389,9 +402,17 @@ cudaError_t launch_integrate_push(const double* q_in, double* q_out, const doubl
     return cudaGetLastError();
 }
 
-cudaError_t launch_md_decide(const double* disp, double margin, cudaGraphConditionalHandle h, int64_t* status,
-                             cudaStream_t s) {
-    k_md_decide<<<1, 1, 0, s>>>(disp, margin, h, status);
+__global__ void k_copy_scalar(const double* __restrict__ src, double* dst) { dst[0] = src[0]; }
+
+cudaError_t launch_copy_scalar(const double* src, double* dst, cudaStream_t s) {
+    k_copy_scalar<<<1, 1, 0, s>>>(src, dst);
+    g_launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_md_decide(const double* disp, int count, int64_t stride, double margin,
+                             cudaGraphConditionalHandle h, int64_t* status, cudaStream_t s) {
+    k_md_decide<<<1, 1, 0, s>>>(disp, count, stride, margin, h, status);
     g_launches++;
     return cudaGetLastError();
 }
@@ -426,8 +447,8 @@ cudaError_t launch_energy(const double* q, const double* p, int64_t row_begin, i
     if (e != cudaSuccess || rows <= 0) return e;
     double rc6 = rc2 * rc2 * rc2;
     double vc = 4.0 * (1.0 / (rc6 * rc6) - 1.0 / rc6);
-    k_energy<<<grid_for(rows, kThreads, 148 * 8), kThreads, 0, s>>>((const rec4*)q, (const rec4*)p, row_begin, rows,
-                                                                   npart, ptr, list, L, rc2, vc, half, out);
+    k_energy<<<grid_for(rows * kEnergyLanes, kThreads, 148 * 8), kThreads, 0, s>>>(
+        (const rec4*)q, (const rec4*)p, row_begin, rows, npart, ptr, list, L, rc2, vc, half, out);
     g_launches++;
     return cudaGetLastError();
 }

@@ -31,6 +31,7 @@ EXPORTS = (
     "lj_gather_probe",
     "lj_list_cell_starts", "lj_force_step_half_cells",
     "lj_md_graph_create", "lj_md_graph_launch", "lj_md_graph_force_ms", "lj_md_graph_kernels", "lj_md_graph_destroy",
+    "lj_md_capture_rebuild", "lj_publish_scalar",
     "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
     "lj_integrate_push", "lj_ipc_get_handle", "lj_ipc_open", "lj_ipc_close",
     "lj_wrap",
@@ -72,6 +73,16 @@ class MDGraphDesc(ctypes.Structure):
                 ("energy_every", ctypes.c_int), ("energies", ctypes.c_void_p)]
 
 
+class MDRebuildDesc(ctypes.Structure):
+    """lj_md_rebuild_desc (include/liblj.h)."""
+    _fields_ = [("q", ctypes.c_void_p), ("q_ref", ctypes.c_void_p), ("n", ctypes.c_int64), ("g", Geom),
+                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("number_of_partners", ctypes.c_void_p), ("pointer", ctypes.c_void_p),
+                ("sorted_list", ctypes.c_void_p), ("capacity", ctypes.c_int64), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t), ("disp", ctypes.c_void_p), ("disp_count", ctypes.c_int),
+                ("disp_stride", ctypes.c_int64), ("status", ctypes.c_void_p)]
+
+
 _lib = None
 
 
@@ -104,6 +115,8 @@ def load() -> ctypes.CDLL:
         "lj_list_cell_starts": (st, [vp, sz, i64, Geom, vp, vp]),
         "lj_md_graph_create": (st, [ctypes.POINTER(MDGraphDesc), ctypes.POINTER(vp)]),
         "lj_md_graph_launch": (st, [vp, vp]),
+        "lj_md_capture_rebuild": (st, [ctypes.POINTER(MDRebuildDesc), vp, ctypes.POINTER(ctypes.c_longlong)]),
+        "lj_publish_scalar": (st, [vp, vp, vp]),
         "lj_md_graph_force_ms": (st, [vp, ctypes.POINTER(ctypes.c_float), i32]),
         "lj_md_graph_kernels": (st, [vp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
         "lj_md_graph_destroy": (st, [vp]),
@@ -434,6 +447,33 @@ class MDGraph:
             self.close()
         except Exception:  # noqa: BLE001 -- interpreter shutdown
             pass
+
+
+def md_capture_rebuild(q: torch.Tensor, q_ref: torch.Tensor, g: Geom, builder: "ListBuilder",
+                       disp: torch.Tensor, disp_count: int, disp_stride: int, status: torch.Tensor) -> int:
+    """lj_md_capture_rebuild on the current (capturing) stream: the device-side bookkeeping
+    decision + an IF node whose body wraps q (q_ref = q) and rebuilds builder's own rows
+    (padded layout).  disp: a float64 CUDA tensor; the decision reads disp.data_ptr()
+    [k * disp_stride] for k < disp_count.  Returns the kernels per rebuild."""
+    _rec(q, "q")
+    _rec(q_ref, "q_ref")
+    if not builder.padded:
+        raise ValueError("md_capture_rebuild: needs the padded list layout")
+    d = MDRebuildDesc(_ptr(q).value, _ptr(q_ref).value, q.shape[0], g, builder.row_begin, builder.row_end,
+                      _ptr(builder.npart).value, _ptr(builder.pointer).value, _ptr(builder.sorted_list).value,
+                      builder.sorted_list.numel(), _ptr(builder.workspace).value, builder.workspace.numel(),
+                      _ptr(disp).value, int(disp_count), int(disp_stride), _ptr(status).value)
+    k = ctypes.c_longlong(0)
+    _check(load().lj_md_capture_rebuild(ctypes.byref(d), _stream(), ctypes.byref(k)))
+    return k.value
+
+
+def publish_scalar(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """lj_publish_scalar: dst[0] = src[0] on the device (float64 CUDA tensors/views)."""
+    for t in (src, dst):
+        if not (t.is_cuda and t.dtype == torch.float64):
+            raise TypeError("publish_scalar: float64 CUDA tensors")
+    _check(load().lj_publish_scalar(_ptr(src), _ptr(dst), _stream()))
 
 
 def force_step_half_cells(q: torch.Tensor, p: torch.Tensor, g: Geom, dt: float, lst: CSRList,

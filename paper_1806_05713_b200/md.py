@@ -152,6 +152,26 @@ class LibBackend:
         lj.energy(q, p, self.g, lst, out)
 
 
+class _TorchGraph:
+    """A torch.cuda.CUDAGraph with the interface StepGraph expects of lj.MDGraph."""
+
+    def __init__(self, graph, steps, kernels_steps, kernels_rebuild):
+        self.graph, self.steps = graph, steps
+        self._k = (kernels_steps, kernels_rebuild)
+
+    def launch(self):
+        self.graph.replay()
+
+    def kernels(self):
+        return self._k
+
+    def force_ms(self):
+        return []   # no per-step event nodes in this graph: the bench times the force kernel separately
+
+    def close(self):
+        self.graph = None
+
+
 @dataclasses.dataclass
 class StepStats:
     rebuilds: int = 0
@@ -549,6 +569,50 @@ class LeapfrogMD:
                        self.q_ref, self.be.perm, self.g, self.dt, self.be.builder, self.disp, self.counter, status,
                        self.reorder, steps, energy_every, energies if ns else None)
         return StepGraph(self, g, status, energy_every, energies if ns else None)
+
+    # ---- the multi-rank step as a CUDA graph (NEXT-1 at P > 1) ----
+    def graph_collective(self, steps: int) -> "StepGraph":
+        """The next `steps` leapfrog steps at P > 1 (or P = 1 with LJ_FORCE_COLLECTIVES=1) as ONE
+        CUDA graph, NCCL included (torch.cuda.graph capture): per step the kick over the own rows,
+        the drift + displacement, the rank's displacement published into the pad lane of its first
+        own q record (lj_publish_scalar), the in-place NCCL all-gather of the positions -- which
+        thereby also carries every rank's displacement -- and the device-side bookkeeping decision
+        over the P pads with the conditional rebuild (lj_md_capture_rebuild: wrap + own-row list,
+        no re-sort).  No host round trip per step or per rebuild.  From here on atoms keep their
+        storage slots (fixed ownership): eager steps of this driver no longer re-sort
+        either, so both paths follow the same trajectory bit for bit."""
+        if not self.collective or self.push or self.halo or self.n % self.world != 0:
+            raise ValueError("graph_collective: NCCL driver with equal slabs and the all-gather exchange only")
+        if not hasattr(self.be, "builder"):
+            raise ValueError("graph_collective: the liblj backend only")
+        torch.cuda.current_stream().synchronize()
+        self.gather_all_positions()
+        self._resolve()
+        if hasattr(self.be, "headroom_ok") and not self.be.headroom_ok():
+            raise lj.LJError(lj.LJ_ERR_UNSUPPORTED, "graph: list rows within %d entries of the padded stride; "
+                             "use eager steps" % self.be.ROW_MARGIN)
+        self.reorder = False
+        self.overlap = False
+        status = torch.zeros(4, dtype=torch.int64, device=self.q.device)
+        n_own = self.n // self.world
+        pads = self.q.view(-1)[3:]                      # pad lane of record 0; rank r's first record at 4 r n_own
+        own_pad = self.q[self.rb, 3:4]
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(device=self.q.device)
+        cs.wait_stream(torch.cuda.current_stream())
+        l0 = lj.launch_count()
+        kpr = 0
+        with torch.cuda.graph(g, stream=cs, capture_error_mode="relaxed"):
+            for _ in range(steps):
+                self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
+                self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, self.rb, self.re, self.disp)
+                lj.publish_scalar(self.disp, own_pad)
+                dist.all_gather_into_tensor(self.q, self.q[self.rb:self.re], group=self.comm)
+                kpr = lj.md_capture_rebuild(self.q, self.q_ref, self.g, self.be.builder, pads, self.world,
+                                            4 * n_own, status)
+        torch.cuda.current_stream().wait_stream(cs)
+        per_step_total = lj.launch_count() - l0 - kpr * steps
+        return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr), status)
 
     def close(self):
         """Unmap the peers' replicas (exchange="push"); the driver is unusable afterwards."""

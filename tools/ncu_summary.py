@@ -45,7 +45,11 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__by
         "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
         "smsp__inst_executed.sum", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_lg_cmd_read.sum", "l1tex__m_xbar2l1tex_read_bytes.sum",
+        "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_bytes.sum"]
 
 
 def full(path):
