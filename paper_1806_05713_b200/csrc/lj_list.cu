@@ -579,6 +579,8 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
 constexpr int kMaxRows = 256;   // atoms per cell handled by v4 (more -> overflow fallback)
 constexpr int kItemRows = 8;    // rows per work item (8: one item per half-cell nearly always -- 8-9 items per cell, one per warp)
 constexpr int kMaxItems = kMaxRows / kItemRows + 8;
+constexpr int kRankPathMaxOverlaps = 40;   // overlapping neighbour-run pairs (of 351) up to which the
+                                           // unsorted staging ranks atoms instead of sorting keys
 
 __device__ __forceinline__ unsigned long long pack_f32x2(float lo, float hi) {
     unsigned long long r;
@@ -641,6 +643,7 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
     __shared__ int s_off[28];
     __shared__ signed char s_dc[27][3];   // neighbour cell offset (-1, 0, 1) per axis
     __shared__ int s_any, s_unsorted, s_next;
+    __shared__ int s_first[27], s_last[27];   // first / last atom index of each neighbour run (rank order)
     __shared__ int s_tlen[8];
     __shared__ float4 s_row[kMaxRows];
     __shared__ unsigned char s_rtau[kMaxRows], s_rk[kMaxRows], s_rowlist[kMaxRows];
@@ -712,8 +715,23 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
             const int prev_last = __shfl_sync(0xffffffffu, rl, prev);
             const unsigned bad = __ballot_sync(0xffffffffu, mycnt > 0 && before != 0 && prev_last > rf);
             const unsigned any = __ballot_sync(0xffffffffu, mine);
+            // how far from sorted: pairs of runs whose index intervals overlap (storage that has
+            // drifted from cell order since the last sort: a few migrants per cell, few overlaps;
+            // shuffled storage: nearly all 351 pairs overlap)
+            int ovl = 0;
+            for (int u = 0; u < 27; u++) {
+                const int fu = __shfl_sync(0xffffffffu, rf, u), lu = __shfl_sync(0xffffffffu, rl, u);
+                const int cu = __shfl_sync(0xffffffffu, mycnt, u);
+                ovl += (lane < 27 && u > lane && mycnt > 0 && cu > 0 && !(lu < rf || fu > rl)) ? 1 : 0;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ovl += __shfl_xor_sync(0xffffffffu, ovl, o);
+            if (lane < 27) {
+                s_first[lane] = mycnt > 0 ? rf : INT_MAX;
+                s_last[lane] = mycnt > 0 ? rl : INT_MIN;
+            }
             if (lane == 0) {
-                s_unsorted = bad != 0;
+                s_unsorted = bad == 0 ? 0 : (ovl <= kRankPathMaxOverlaps ? 1 : 2);
                 s_any = any != 0;
                 s_next = 0;
             }
@@ -746,6 +764,45 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
                     CY[m] = f.y;
                     CZ[m] = f.z;
                     CJ[m] = __float_as_int(f.w);
+                    TM[m] = (unsigned char)type_mask(f, hw, fw, a.rb2);
+                }
+            }
+        } else if (s_unsorted == 1) {
+            // nearly sorted storage: every run is ascending (cells sorted by k_cell_sort_gather),
+            // so an atom's slot in the ascending staging order is its position in its own run +
+            // the atoms of the other runs below it -- whole runs by their [first, last] interval,
+            // a binary search only for the few runs whose interval straddles it.  No sort, no
+            // barrier; the staged order is the same as the sorted one.
+            for (int t = w; t < 27; t += kListWarps) {
+                const int n = s_off[t + 1] - s_off[t];
+                const float sx = s_dc[t][0] * fw, sy = s_dc[t][1] * fw, sz = s_dc[t][2] * fw;
+                const float4* src = a.qr_cell + s_start[t];
+                for (int k = lane; k < n; k += 32) {
+                    float4 f = src[k];
+                    const int x = __float_as_int(f.w);
+                    int m = k;
+                    for (int u = 0; u < 27; u++) {
+                        if (u == t || x < s_first[u]) continue;
+                        const int nu = s_off[u + 1] - s_off[u];
+                        if (x > s_last[u]) {
+                            m += nu;
+                        } else {   // x inside run u's interval: count its atoms below x
+                            const int32_t* ru = a.atoms + s_start[u];
+                            int lo = 0, hi = nu;
+                            while (lo < hi) {
+                                const int mid = (lo + hi) >> 1;
+                                if (ru[mid] < x) lo = mid + 1; else hi = mid;
+                            }
+                            m += lo;
+                        }
+                    }
+                    f.x += sx;
+                    f.y += sy;
+                    f.z += sz;
+                    CX[m] = f.x;
+                    CY[m] = f.y;
+                    CZ[m] = f.z;
+                    CJ[m] = x;
                     TM[m] = (unsigned char)type_mask(f, hw, fw, a.rb2);
                 }
             }

@@ -742,3 +742,31 @@ def test_overflowed_padded_list_stays_in_bounds(lj, dev):
     assert st[0] >= 1 and st[1] == 1              # rebuilt, overflow flagged
     assert int(b.npart.max().item()) == S
     gr.close()
+
+
+@pytest.mark.parametrize("drift", [0.05, 0.15, 0.4, 1.5])
+@pytest.mark.parametrize("half", [False, True])
+def test_list_storage_drifted_from_cell_order(lj, dev, systems, drift, half):
+    """Storage sorted into cell order once, then atoms moved (fixed row ownership, as
+    the multi-rank graph keeps it): cells hold a few atoms whose indices lie in other
+    cells' ranges.  The builder ranks the candidates by run intervals (few overlaps) or
+    sorts their keys (many) -- the pair set and the ascending rows stay the oracle's."""
+    w = systems[3]
+    rng = np.random.default_rng(int(drift * 100) + half)
+    q = lj_inputs.wrap_into_box(w.q + rng.uniform(-drift, drift, w.q.shape), w.L)
+    g = lj.geom(w.L, w.rc, w.rs)
+    for padded in (False, True):
+        b = lj.ListBuilder(w.n, g, half, device=dev, padded=padded)
+        gl = b.build(to_dev(q, dev))
+        ol = oracle.list_cells(q, w.L, w.rs, half)
+        if padded:
+            n_e = ol.n_entries
+            assert gl.n_entries == n_e
+            assert np.array_equal(gl.number_of_partners.cpu().numpy(), ol.number_of_partners)
+            S = lj.LJ_PADDED_ROW_STRIDE
+            rows = gl.sorted_list[: w.n * S].view(w.n, S).cpu().numpy()
+            for i in range(0, w.n, 97):   # sampled rows: identical, ascending
+                k = ol.number_of_partners[i]
+                assert np.array_equal(rows[i, :k], ol.sorted_list[ol.pointer[i]:ol.pointer[i] + k])
+        else:
+            assert_same_list(gl, ol)

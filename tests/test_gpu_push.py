@@ -128,3 +128,33 @@ def test_push_through_cuda_ipc(lj, tmp_path):
     lo, hi = 3_000, 7_500
     assert np.array_equal(got[lo:hi], sent[lo:hi])
     assert (got[:lo] == -1.0).all() and (got[hi:] == -1.0).all()
+
+
+def test_push_against_the_oracle(lj):
+    """the fused drift + push compared with the ORACLE directly (reading
+    O6 integrate, C-16 displacement): own rows, every pushed replica row and the
+    maximum displacement bit-identical to oracle.integrate / oracle.max_displacement."""
+    import oracle
+    rng = np.random.default_rng(23)
+    n, dt = 20_000, 0.005
+    qn = rng.uniform(0, 30, (n, 3))
+    pn = rng.normal(0, 1, (n, 3))
+    qrefn = qn + rng.normal(0, 0.05, (n, 3))
+    b, e = 4_000, 13_333
+    q = lj.pack_aos4(torch.from_numpy(qn).cuda())
+    p = lj.pack_aos4(torch.from_numpy(pn).cuda())
+    q_ref = lj.pack_aos4(torch.from_numpy(qrefn).cuda())
+    peers = [torch.zeros((n, 4), dtype=torch.float64, device="cuda") for _ in range(2)]
+    ranges = [(b, b + 700), (e - 1500, e)]
+    q_out = torch.zeros_like(q)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    lj.integrate_push(q, q_out, p, q_ref, dt, b, e, out,
+                      [(t.data_ptr(), lo, hi) for t, (lo, hi) in zip(peers, ranges)])
+    torch.cuda.synchronize()
+    ref = oracle.integrate(qn, pn, dt, b, e)
+    got = q_out[:, :3].cpu().numpy()
+    assert np.array_equal(got[b:e], ref[b:e])
+    for t, (lo, hi) in zip(peers, ranges):
+        assert np.array_equal(t[lo:hi, :3].cpu().numpy(), ref[lo:hi])
+        assert not t[:lo].any() and not t[hi:].any()
+    assert out.item() == oracle.max_displacement(ref, qrefn, b, e)
