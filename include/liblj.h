@@ -384,6 +384,16 @@ typedef struct {
     int disp_count;           /* pads of every rank's first q record after the all-gather (see */
     int64_t disp_stride;      /* lj_publish_scalar), or one all-reduced double (count 1, stride 0) */
     int64_t *status;          /* 4 int64, as lj_md_graph_desc.status */
+    int reorder;              /* re-sort all atoms into cell order at every rebuild (as lj_rebuild); the own
+                                 rows then change owner-rank, their momenta are read from p_peers: */
+    double *q_alt;            /* n records: scratch */
+    double *p;                /* n records: this rank's momenta (own rows [row_begin, row_end) valid) */
+    double *p_alt;            /* n records: scratch */
+    int64_t *perm;            /* n: scratch */
+    const double *const *p_peers; /* DEVICE array of P pointers: rank k's copy of its own rows' momenta
+                                 (n records, rows [k n_own, (k+1) n_own) valid; peer-mapped, e.g. CUDA
+                                 IPC), current when the rebuild runs -- see lj_copy_records */
+    int64_t n_own;            /* rows per rank (equal slabs; own rows = one slab) */
 } lj_md_rebuild_desc;
 
 /* Called while `stream` is being captured into a CUDA graph (cudaStreamBeginCapture
@@ -391,11 +401,28 @@ typedef struct {
  * collectives): appends to the capture a one-thread kernel that takes the
  * bookkeeping decision (rebuild iff 2 max_k disp[k*stride] >= rs - rc, reading
  * C-16) and an IF node whose body wraps all n records of q
- * (q_ref = the wrapped q, as lj_wrap) and rebuilds the own rows' padded list
- * (as lj_build_list_ex, status to d->status as lj_md_graph).  Work captured
+ * (q_ref = the wrapped q, as lj_wrap) -- with reorder, also re-sorts every atom
+ * into cell order (as lj_permute_rows_peers, the permuted q / own p copied back
+ * into q / p) -- and rebuilds the own rows' padded list (as lj_build_list_ex,
+ * status to d->status as lj_md_graph).  Work captured
  * afterwards on `stream` depends on the IF node.  *kernels_per_rebuild (if not
  * NULL) = kernels the body launches.  LJ_ERR_ARG if `stream` is not capturing. */
 lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc *d, void *stream, long long *kernels_per_rebuild);
+
+/* dst[k] = src[k] for n records (device, stream-ordered; src == dst is a no-op): e.g. a
+ * rank's own momenta into the buffer its peers read at a re-sorting rebuild. */
+lj_status lj_copy_records(const double *src, double *dst, int64_t n, void *stream);
+
+/* The multi-rank re-sort on its own (lj_rebuild's cell pass without the list):
+ * q (n records, replicated) is wrapped in place, perm[new] = old is the stable
+ * cell order, q_out = q permuted, q_ref = q_out (if not NULL), and for the own
+ * new rows [own_lo, own_hi) p_out[k] = p_peers[perm[k] / n_own][perm[k]] -- the
+ * momenta read from the rank that owned the atom (device table of P pointers,
+ * peer-mapped).  Rows of p_out outside [own_lo, own_hi) are not written. */
+lj_status lj_permute_rows_peers(double *q, double *q_out, double *q_ref, double *p_out,
+                                const double *const *p_peers, int64_t n_own, int64_t own_lo, int64_t own_hi,
+                                int64_t *perm, int64_t n, lj_geom g, void *workspace, size_t workspace_bytes,
+                                void *stream);
 
 /* dst[0] = src[0] (device doubles), stream-ordered: e.g. the rank's maximum
  * displacement into the pad lane of its first own q record, which the position

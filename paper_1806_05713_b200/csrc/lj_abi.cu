@@ -135,6 +135,7 @@ struct RebuildIO {
     const double* p;
     double *q_out, *p_out, *q_ref;
     int64_t* perm;
+    PeerMomenta pm;   // momenta from every rank's copy of its own rows (multi-rank re-sort), else p
 };
 
 lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64_t row_begin, int64_t row_end,
@@ -168,7 +169,7 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
     }
     int64_t* counts_scan = padded ? (int64_t*)(ws + W.off_ptrtmp) : pointer;
     if (rb)
-        LJ_CUDA(launch_rebuild_cells(rb->q, rb->p, rb->q_out, rb->p_out, rb->q_ref, rb->perm, n, cg, ws, W, s),
+        LJ_CUDA(launch_rebuild_cells(rb->q, rb->p, rb->q_out, rb->p_out, rb->q_ref, rb->perm, n, cg, ws, W, s, rb->pm),
                 "lj_rebuild/cells");
     else
         LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
@@ -242,7 +243,7 @@ lj_status lj_rebuild(double* q, const double* p, double* q_out, double* p_out, d
         return fail(LJ_ERR_ARG, "rebuild: output buffers must be distinct from the inputs and each other");
     if (!aligned32(q) || !aligned32(q_out) || !aligned32(p) || !aligned32(p_out) || !aligned32(q_ref))
         return fail(LJ_ERR_ARG, "rebuild: records not 32-byte aligned");
-    RebuildIO io{q, p, q_out, p_out, q_ref, perm};
+    RebuildIO io{q, p, q_out, p_out, q_ref, perm, PeerMomenta()};
     return build_list_impl(q_out, n, g, half, row_begin, row_end, flags, number_of_partners, pointer, sorted_list,
                            capacity, n_entries, workspace, workspace_bytes, stream, &io);
 }
@@ -687,7 +688,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
         l0 = g_launches;
         lj_status st = LJ_OK;
         if (d->reorder) {   // as lj_rebuild, then the permuted state back into q / p
-            RebuildIO io{d->q, d->p, d->q_alt, d->p_alt, d->q_ref, d->perm};
+            RebuildIO io{d->q, d->p, d->q_alt, d->p_alt, d->q_ref, d->perm, PeerMomenta()};
             st = build_list_impl(d->q_alt, n, d->g, 0, 0, n, LJ_LIST_PADDED, d->number_of_partners, d->pointer,
                                  d->sorted_list, d->capacity, d->status + 2, d->workspace, d->workspace_bytes, cs,
                                  &io, d->status);
@@ -727,6 +728,16 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long 
     if (!aligned32(d->q) || !aligned32(d->q_ref)) return fail(LJ_ERR_ARG, "md_capture_rebuild: records not 32-byte aligned");
     if (d->disp_count < 1 || d->disp_count > 4096 || d->disp_stride < 0)
         return fail(LJ_ERR_ARG, "md_capture_rebuild: need 1 <= disp_count <= 4096, disp_stride >= 0");
+    if (d->reorder) {
+        if (!d->q_alt || !d->p || !d->p_alt || !d->perm || !d->p_peers)
+            return fail(LJ_ERR_ARG, "md_capture_rebuild: reorder needs q_alt, p, p_alt, perm and p_peers");
+        if (!aligned32(d->q_alt) || !aligned32(d->p) || !aligned32(d->p_alt))
+            return fail(LJ_ERR_ARG, "md_capture_rebuild: records not 32-byte aligned");
+        if (d->n_own < 1 || n % d->n_own != 0 || d->row_begin % d->n_own != 0 || d->row_end - d->row_begin != d->n_own)
+            return fail(LJ_ERR_ARG, "md_capture_rebuild: reorder needs equal slabs (n_own divides n, own rows = "
+                        "one slab)");
+        if (d->q_alt == d->q || d->p_alt == d->p) return fail(LJ_ERR_ARG, "md_capture_rebuild: alt buffers must differ");
+    }
     const int64_t rows = d->row_end - d->row_begin;
     if (d->capacity < rows * (int64_t)LJ_PADDED_ROW_STRIDE)
         return fail(LJ_ERR_CAPACITY, "md_capture_rebuild: the padded list needs capacity %lld",
@@ -763,11 +774,30 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long 
     const long long l0 = g_launches;
     lj_status st = LJ_OK;
     if (e == cudaSuccess) {
-        e = launch_wrap(d->q, d->q_ref, n, d->g.L, bs);
-        if (e == cudaSuccess)
-            st = build_list_impl(d->q, n, d->g, 0, d->row_begin, d->row_end, LJ_LIST_PADDED, d->number_of_partners,
-                                 d->pointer, d->sorted_list, d->capacity, d->status + 2, d->workspace,
-                                 d->workspace_bytes, bs, nullptr, d->status);
+        if (d->reorder) {
+            // as lj_rebuild -- wrap, cells, the cell-order permutation of q (replicated) and q_ref --
+            // with the own new rows' momenta read from the rank that owned each atom (d->p_peers,
+            // NVLink loads of the peers' copies), then the permuted state back into q / own p rows
+            RebuildIO io{d->q, nullptr, d->q_alt, d->p_alt, d->q_ref, d->perm, PeerMomenta()};
+            io.pm.table = d->p_peers;
+            io.pm.n_own = d->n_own;
+            io.pm.own_lo = d->row_begin;
+            io.pm.own_hi = d->row_end;
+            st = build_list_impl(d->q_alt, n, d->g, 0, d->row_begin, d->row_end, LJ_LIST_PADDED,
+                                 d->number_of_partners, d->pointer, d->sorted_list, d->capacity, d->status + 2,
+                                 d->workspace, d->workspace_bytes, bs, &io, d->status);
+            const size_t rec = sizeof(double) * 4;
+            if (st == LJ_OK) e = cudaMemcpyAsync(d->q, d->q_alt, rec * (size_t)n, cudaMemcpyDeviceToDevice, bs);
+            if (st == LJ_OK && e == cudaSuccess)
+                e = cudaMemcpyAsync(d->p + 4 * d->row_begin, d->p_alt + 4 * d->row_begin,
+                                    rec * (size_t)(d->row_end - d->row_begin), cudaMemcpyDeviceToDevice, bs);
+        } else {
+            e = launch_wrap(d->q, d->q_ref, n, d->g.L, bs);
+            if (e == cudaSuccess)
+                st = build_list_impl(d->q, n, d->g, 0, d->row_begin, d->row_end, LJ_LIST_PADDED,
+                                     d->number_of_partners, d->pointer, d->sorted_list, d->capacity, d->status + 2,
+                                     d->workspace, d->workspace_bytes, bs, nullptr, d->status);
+        }
         cudaGraph_t tmp;
         const cudaError_t e2 = cudaStreamEndCapture(bs, &tmp);
         if (e == cudaSuccess) e = e2;
@@ -779,6 +809,41 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long 
     // later captured work on `stream` follows the IF node
     LJ_CUDA(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies),
             "md_capture_rebuild/deps");
+    return LJ_OK;
+}
+
+lj_status lj_copy_records(const double* src, double* dst, int64_t n, void* stream) {
+    if (n < 0 || (n > 0 && (!src || !dst))) return fail(LJ_ERR_ARG, "copy_records: bad argument");
+    if (!aligned32(src) || !aligned32(dst)) return fail(LJ_ERR_ARG, "copy_records: not 32-byte aligned");
+    if (n == 0 || src == dst) return LJ_OK;
+    LJ_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * 4 * (size_t)n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+            "lj_copy_records");
+    return LJ_OK;
+}
+
+lj_status lj_permute_rows_peers(double* q, double* q_out, double* q_ref, double* p_out,
+                                const double* const* p_peers, int64_t n_own, int64_t own_lo, int64_t own_hi,
+                                int64_t* perm, int64_t n, lj_geom g, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+    LJ_TRY(check_n(n));
+    LJ_TRY(check_geom(g, true));
+    if (n > 0 && (!q || !q_out || !p_out || !p_peers || !perm)) return fail(LJ_ERR_ARG, "permute_rows_peers: null pointer");
+    if (!aligned32(q) || !aligned32(q_out) || !aligned32(q_ref) || !aligned32(p_out))
+        return fail(LJ_ERR_ARG, "permute_rows_peers: records not 32-byte aligned");
+    if (n_own < 1 || n % n_own != 0 || own_lo < 0 || own_lo > own_hi || own_hi > n)
+        return fail(LJ_ERR_ARG, "permute_rows_peers: need n_own dividing n and 0 <= own_lo <= own_hi <= n");
+    if (q_out == q) return fail(LJ_ERR_ARG, "permute_rows_peers: q_out must differ from q");
+    const CellGrid cg = make_grid(g);
+    const BuildWorkspace W = build_workspace_layout(n, cg.ncell, n);
+    if (!workspace || workspace_bytes < W.total) return fail(LJ_ERR_ARG, "permute_rows_peers: workspace too small");
+    PeerMomenta pm;
+    pm.table = p_peers;
+    pm.n_own = n_own;
+    pm.own_lo = own_lo;
+    pm.own_hi = own_hi;
+    LJ_CUDA(launch_rebuild_cells(q, nullptr, q_out, p_out, q_ref, perm, n, cg, (char*)workspace, W,
+                                 (cudaStream_t)stream, pm),
+            "lj_permute_rows_peers");
     return LJ_OK;
 }
 

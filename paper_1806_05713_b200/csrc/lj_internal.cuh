@@ -50,9 +50,16 @@ cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* w
                          cudaStream_t s);
 // lj_rebuild: wrap q in place, cells, and the cell-order permutation applied to q/p (q_out, p_out, q_ref), with
 // the builder's staging arrays prepared for the permuted system
+// Momenta source of the re-sort: either p (all n records valid), or -- the multi-rank step,
+// a device table of P pointers to every rank's copy of its own rows
+// (peer-mapped over NVLink), rank = atom / n_own; only p_out rows [own_lo, own_hi) are written.
+struct PeerMomenta {
+    const double* const* table = nullptr;
+    int64_t n_own = 0, own_lo = 0, own_hi = 0;
+};
 cudaError_t launch_rebuild_cells(double* q, const double* p, double* q_out, double* p_out, double* q_ref,
                                  int64_t* perm, int64_t n, const CellGrid& cg, char* ws, const BuildWorkspace& W,
-                                 cudaStream_t s);
+                                 cudaStream_t s, const PeerMomenta& pm = PeerMomenta());
 // pass 1: every row into the per-row scratch (stride kRowCap), counts into npart
 // (out == nullptr: the workspace scratch; else the caller's padded list)
 cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,

@@ -199,7 +199,7 @@ __global__ void k_cell_sort_permute(const rec4* __restrict__ q, const rec4* __re
                                     const int64_t* __restrict__ start, int32_t* __restrict__ atoms,
                                     int64_t* __restrict__ perm, rec4* __restrict__ q_out, rec4* __restrict__ p_out,
                                     rec4* __restrict__ q_ref, rec4* __restrict__ q_cell,
-                                    float4* __restrict__ qr_cell, double cw) {
+                                    float4* __restrict__ qr_cell, double cw, PeerMomenta pm) {
     const int64_t ncell = cg.ncell;
     __shared__ int buf[kListWarps][kCellBuf];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -234,7 +234,12 @@ __global__ void k_cell_sort_permute(const rec4* __restrict__ q, const rec4* __re
             q_out[g] = r;
             q_cell[g] = r;
             if (q_ref) q_ref[g] = r;
-            if (p) p_out[g] = p[i];
+            if (pm.table) {   // own new rows only: the momenta from the rank that owned atom i
+                if (g >= pm.own_lo && g < pm.own_hi)
+                    p_out[g] = reinterpret_cast<const rec4*>(pm.table[i / pm.n_own])[i];   // (coherent load: peer memory)
+            } else if (p) {
+                p_out[g] = p[i];
+            }
             qr_cell[g] = make_float4((float)(r.x - ox), (float)(r.y - oy), (float)(r.z - oz), __int_as_float((int)g));
         }
         __syncwarp();
@@ -1231,7 +1236,7 @@ cudaError_t launch_cells(const double* q, int64_t n, const CellGrid& cg, char* w
 
 cudaError_t launch_rebuild_cells(double* q, const double* p, double* q_out, double* p_out, double* q_ref,
                                  int64_t* perm, int64_t n, const CellGrid& cg, char* ws, const BuildWorkspace& W,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, const PeerMomenta& pm) {
     int32_t* cell_of = (int32_t*)(ws + W.off_cell_of);
     int32_t* count = (int32_t*)(ws + W.off_count);
     int64_t* start = (int64_t*)(ws + W.off_start);
@@ -1252,7 +1257,7 @@ cudaError_t launch_rebuild_cells(double* q, const double* p, double* q_out, doub
         k_cell_scatter<<<grid_for(n, 256), 256, 0, s>>>(n, cell_of, start, cursor, atoms);
         k_cell_sort_permute<<<grid_for(cg.ncell, kListWarps), kListWarps * 32, 0, s>>>(
             (const rec4*)q, (const rec4*)p, cg, start, atoms, perm, (rec4*)q_out, (rec4*)p_out, (rec4*)q_ref,
-            (rec4*)(ws + W.off_qcell), (float4*)(ws + W.off_qr), cg.L / cg.nc);
+            (rec4*)(ws + W.off_qcell), (float4*)(ws + W.off_qr), cg.L / cg.nc, pm);
         g_launches += 2;
     }
     return cudaGetLastError();

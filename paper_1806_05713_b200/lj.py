@@ -31,7 +31,7 @@ EXPORTS = (
     "lj_gather_probe",
     "lj_list_cell_starts", "lj_force_step_half_cells",
     "lj_md_graph_create", "lj_md_graph_launch", "lj_md_graph_force_ms", "lj_md_graph_kernels", "lj_md_graph_destroy",
-    "lj_md_capture_rebuild", "lj_publish_scalar",
+    "lj_md_capture_rebuild", "lj_copy_records", "lj_permute_rows_peers", "lj_publish_scalar",
     "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
     "lj_integrate_push", "lj_ipc_get_handle", "lj_ipc_open", "lj_ipc_close",
     "lj_wrap",
@@ -80,7 +80,9 @@ class MDRebuildDesc(ctypes.Structure):
                 ("number_of_partners", ctypes.c_void_p), ("pointer", ctypes.c_void_p),
                 ("sorted_list", ctypes.c_void_p), ("capacity", ctypes.c_int64), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t), ("disp", ctypes.c_void_p), ("disp_count", ctypes.c_int),
-                ("disp_stride", ctypes.c_int64), ("status", ctypes.c_void_p)]
+                ("disp_stride", ctypes.c_int64), ("status", ctypes.c_void_p), ("reorder", ctypes.c_int),
+                ("q_alt", ctypes.c_void_p), ("p", ctypes.c_void_p), ("p_alt", ctypes.c_void_p),
+                ("perm", ctypes.c_void_p), ("p_peers", ctypes.c_void_p), ("n_own", ctypes.c_int64)]
 
 
 _lib = None
@@ -117,6 +119,8 @@ def load() -> ctypes.CDLL:
         "lj_md_graph_launch": (st, [vp, vp]),
         "lj_md_capture_rebuild": (st, [ctypes.POINTER(MDRebuildDesc), vp, ctypes.POINTER(ctypes.c_longlong)]),
         "lj_publish_scalar": (st, [vp, vp, vp]),
+        "lj_copy_records": (st, [vp, vp, i64, vp]),
+        "lj_permute_rows_peers": (st, [vp, vp, vp, vp, vp, i64, i64, i64, vp, i64, Geom, vp, sz, vp]),
         "lj_md_graph_force_ms": (st, [vp, ctypes.POINTER(ctypes.c_float), i32]),
         "lj_md_graph_kernels": (st, [vp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
         "lj_md_graph_destroy": (st, [vp]),
@@ -156,6 +160,10 @@ def _stream():
 
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _addr(t):
+    return None if t is None else t.data_ptr()
 
 
 def _rec(t, name):
@@ -450,22 +458,58 @@ class MDGraph:
 
 
 def md_capture_rebuild(q: torch.Tensor, q_ref: torch.Tensor, g: Geom, builder: "ListBuilder",
-                       disp: torch.Tensor, disp_count: int, disp_stride: int, status: torch.Tensor) -> int:
+                       disp: torch.Tensor, disp_count: int, disp_stride: int, status: torch.Tensor,
+                       resort: dict | None = None) -> int:
     """lj_md_capture_rebuild on the current (capturing) stream: the device-side bookkeeping
-    decision + an IF node whose body wraps q (q_ref = q) and rebuilds builder's own rows
-    (padded layout).  disp: a float64 CUDA tensor; the decision reads disp.data_ptr()
-    [k * disp_stride] for k < disp_count.  Returns the kernels per rebuild."""
+    decision + an IF node whose body wraps q (q_ref = q), optionally re-sorts every atom into
+    cell order (resort = dict(q_alt, p, p_alt, perm, p_peers (int64 CUDA tensor of P device
+    pointers), n_own)), and rebuilds builder's own rows (padded layout).  disp: a float64
+    CUDA tensor; the decision reads disp.data_ptr()[k * disp_stride] for k < disp_count.
+    Returns the kernels per rebuild."""
     _rec(q, "q")
     _rec(q_ref, "q_ref")
     if not builder.padded:
         raise ValueError("md_capture_rebuild: needs the padded list layout")
+    r = resort or {}
+    if resort is not None:
+        for name in ("q_alt", "p", "p_alt"):
+            _rec(r[name], name)
+        if not (r["p_peers"].is_cuda and r["p_peers"].dtype == torch.int64):
+            raise TypeError("md_capture_rebuild: p_peers must be a CUDA int64 tensor of device pointers")
     d = MDRebuildDesc(_ptr(q).value, _ptr(q_ref).value, q.shape[0], g, builder.row_begin, builder.row_end,
                       _ptr(builder.npart).value, _ptr(builder.pointer).value, _ptr(builder.sorted_list).value,
                       builder.sorted_list.numel(), _ptr(builder.workspace).value, builder.workspace.numel(),
-                      _ptr(disp).value, int(disp_count), int(disp_stride), _ptr(status).value)
+                      _ptr(disp).value, int(disp_count), int(disp_stride), _ptr(status).value,
+                      int(resort is not None), _addr(r.get("q_alt")), _addr(r.get("p")), _addr(r.get("p_alt")),
+                      _addr(r.get("perm")), _addr(r.get("p_peers")), int(r.get("n_own", 0)))
     k = ctypes.c_longlong(0)
     _check(load().lj_md_capture_rebuild(ctypes.byref(d), _stream(), ctypes.byref(k)))
     return k.value
+
+
+def copy_records(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """lj_copy_records: dst[:] = src[:] (n AoS4 records, device, stream-ordered)."""
+    _rec(src, "src")
+    _rec(dst, "dst")
+    if src.shape[0] != dst.shape[0]:
+        raise ValueError("copy_records: shapes differ")
+    _check(load().lj_copy_records(_ptr(src), _ptr(dst), src.shape[0], _stream()))
+
+
+def permute_rows_peers(q: torch.Tensor, q_out: torch.Tensor, q_ref: torch.Tensor | None, p_out: torch.Tensor,
+                       p_peers: torch.Tensor, n_own: int, own_lo: int, own_hi: int, perm: torch.Tensor, g: Geom,
+                       workspace: torch.Tensor) -> None:
+    """lj_permute_rows_peers: the multi-rank re-sort (q wrapped in place; perm, q_out, q_ref and
+    the own new rows of p_out, their momenta read from the owner ranks' buffers p_peers)."""
+    for t, name in ((q, "q"), (q_out, "q_out"), (p_out, "p_out")):
+        _rec(t, name)
+    if q_ref is not None:
+        _rec(q_ref, "q_ref")
+    if not (p_peers.is_cuda and p_peers.dtype == torch.int64):
+        raise TypeError("permute_rows_peers: p_peers must be a CUDA int64 tensor of device pointers")
+    _check(load().lj_permute_rows_peers(_ptr(q), _ptr(q_out), _ptr(q_ref), _ptr(p_out), _ptr(p_peers), int(n_own),
+                                        int(own_lo), int(own_hi), _ptr(perm), q.shape[0], g, _ptr(workspace),
+                                        workspace.numel(), _stream()))
 
 
 def publish_scalar(src: torch.Tensor, dst: torch.Tensor) -> None:

@@ -571,51 +571,101 @@ class LeapfrogMD:
         return StepGraph(self, g, status, energy_every, energies if ns else None)
 
     # ---- the multi-rank step as a CUDA graph (NEXT-1 at P > 1) ----
-    def graph_collective(self, steps: int) -> "StepGraph":
+    def graph_collective(self, steps: int, resort: bool | None = None) -> "StepGraph":
         """The next `steps` leapfrog steps at P > 1 (or P = 1 with LJ_FORCE_COLLECTIVES=1) as ONE
-        CUDA graph, NCCL included (torch.cuda.graph capture): per step the kick over the own rows,
-        the drift + displacement, the rank's displacement published into the pad lane of its first
-        own q record (lj_publish_scalar), the in-place NCCL all-gather of the positions -- which
+        CUDA graph, NCCL included (torch.cuda.graph capture).  Per step: the kick over the own rows;
+        the drift + displacement; the own momenta copied into this step's share buffer (two,
+        alternating by step parity); the rank's displacement published into the pad lane of its
+        first own q record (lj_publish_scalar); the in-place NCCL all-gather of the positions -- which
         thereby also carries every rank's displacement -- and the device-side bookkeeping decision
-        over the P pads with the conditional rebuild (lj_md_capture_rebuild: wrap + own-row list,
-        no re-sort).  No host round trip per step or per rebuild.  From here on atoms keep their
-        storage slots (fixed ownership): eager steps of this driver no longer re-sort
-        either, so both paths follow the same trajectory bit for bit."""
+        over the P pads with the conditional rebuild (lj_md_capture_rebuild).  With resort (default:
+        the driver's reorder), the rebuild re-sorts every atom into cell order as lj_rebuild does and
+        reads the own new rows' momenta straight from the owner ranks' share buffers over NVLink
+        (CUDA IPC mappings) -- no host round trip per step or per rebuild, no momentum
+        collective.  Without resort, atoms keep their storage slots (fixed ownership).  Either way
+        the eager steps of this driver follow the same trajectory bit for bit.
+
+        Ordering of the share buffers: rank r writes share[k % 2] in step k before its all-gather k;
+        a peer reads it only in the rebuild of step k, after all-gather k has completed there; r next
+        writes share[k % 2] in step k + 2, after all-gather k + 1 -- which the peer joins only once
+        its rebuild of step k is done (stream order)."""
         if not self.collective or self.push or self.halo or self.n % self.world != 0:
             raise ValueError("graph_collective: NCCL driver with equal slabs and the all-gather exchange only")
         if not hasattr(self.be, "builder"):
             raise ValueError("graph_collective: the liblj backend only")
+        resort = self.reorder if resort is None else bool(resort)
         torch.cuda.current_stream().synchronize()
         self.gather_all_positions()
         self._resolve()
         if hasattr(self.be, "headroom_ok") and not self.be.headroom_ok():
             raise lj.LJError(lj.LJ_ERR_UNSUPPORTED, "graph: list rows within %d entries of the padded stride; "
                              "use eager steps" % self.be.ROW_MARGIN)
-        self.reorder = False
+        self.reorder = resort
         self.overlap = False
         status = torch.zeros(4, dtype=torch.int64, device=self.q.device)
         n_own = self.n // self.world
         pads = self.q.view(-1)[3:]                      # pad lane of record 0; rank r's first record at 4 r n_own
         own_pad = self.q[self.rb, 3:4]
+        rs = None
+        if resort:
+            if getattr(self, "q_alt", None) is None:
+                self.q_alt = self.be.empty_records(self.n)
+            if getattr(self, "p_alt", None) is None:
+                self.p_alt = self.be.empty_records(self.n)
+            if getattr(self.be, "perm", None) is None:
+                self.be.perm = torch.empty(self.n, dtype=torch.int64, device=self.q.device)
+            self._p_share, self._p_tables = self._open_momentum_shares()
+            rs = [dict(q_alt=self.q_alt, p=self.p, p_alt=self.p_alt, perm=self.be.perm, p_peers=self._p_tables[b],
+                       n_own=n_own) for b in range(2)]
         g = torch.cuda.CUDAGraph()
         cs = torch.cuda.Stream(device=self.q.device)
         cs.wait_stream(torch.cuda.current_stream())
         l0 = lj.launch_count()
         kpr = 0
         with torch.cuda.graph(g, stream=cs, capture_error_mode="relaxed"):
-            for _ in range(steps):
+            for k in range(steps):
                 self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
                 self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, self.rb, self.re, self.disp)
+                if resort:
+                    lj.copy_records(self.p[self.rb:self.re], self._p_share[k % 2][self.rb:self.re])
                 lj.publish_scalar(self.disp, own_pad)
                 dist.all_gather_into_tensor(self.q, self.q[self.rb:self.re], group=self.comm)
                 kpr = lj.md_capture_rebuild(self.q, self.q_ref, self.g, self.be.builder, pads, self.world,
-                                            4 * n_own, status)
+                                            4 * n_own, status, rs[k % 2] if resort else None)
         torch.cuda.current_stream().wait_stream(cs)
         per_step_total = lj.launch_count() - l0 - kpr * steps
         return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr), status)
 
+    def _open_momentum_shares(self):
+        """Two share buffers for the own momenta and, per buffer, a device table of every rank's
+        buffer pointer (CUDA IPC mappings of the peers' buffers; this rank's own pointer locally)."""
+        shares = [self.be.shared_records(self.n) for _ in range(2)] if hasattr(self.be, "shared_records") \
+            else [self.be.empty_records(self.n) for _ in range(2)]
+        if self.world > 1:
+            mine = [self.be.share(t) for t in shares]
+            table = [None] * self.world
+            dist.all_gather_object(table, mine, group=self.comm)
+            self._share_peers = [[None if a == self.rank else self.be.open_shared(table[a][b])
+                                  for a in range(self.world)] for b in range(2)]
+            ptrs = [[shares[b].data_ptr() if a == self.rank else self._share_peers[b][a] for a in range(self.world)]
+                    for b in range(2)]
+        else:
+            self._share_peers = None
+            ptrs = [[shares[b].data_ptr()] for b in range(2)]
+        tables = [torch.tensor(ptrs[b], dtype=torch.int64, device=self.q.device) for b in range(2)]
+        return shares, tables
+
     def close(self):
-        """Unmap the peers' replicas (exchange="push"); the driver is unusable afterwards."""
+        """Unmap the peers' replicas (exchange="push") and momentum shares (graph_collective);
+        the driver is unusable afterwards."""
+        shares = getattr(self, "_share_peers", None)
+        closer = getattr(self.be, "close_shared", None)
+        if shares is not None and closer is not None:
+            for row in shares:
+                for ptr in row:
+                    if ptr is not None:
+                        closer(ptr)
+            self._share_peers = None
         if self.push and self._peers is not None:
             closer = getattr(self.be, "close_shared", None)
             if closer is not None:

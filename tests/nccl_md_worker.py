@@ -59,25 +59,29 @@ def main():
     out["energy_first10_max_rel"] = float(np.max(np.abs(E[:11] - Er[:11]) / np.abs(Er[:11])))
     out["rebuilds"] = [s.stats.rebuilds, int(rb_ref)]
 
-    # 2. captured multi-rank step == eager NCCL steps, bit for bit (two launches)
-    a, b = sim(reorder=True), sim(reorder=True)    # one initial re-sort, then fixed ownership
-    a.reorder = False
-    n_steps = 30
-    gr = b.graph_collective(n_steps)
-    ok = True
-    for launch in range(2):
-        for _ in range(n_steps):
-            a.kick(w.dt, a.counter)
-            a.drift_and_exchange()
-        gr.launch()
-        torch.cuda.synchronize()
-        gr.finish()
-        ok = ok and torch.equal(a.q[:, :3], b.q[:, :3]) and torch.equal(a.p, b.p)
-        ok = ok and a.stats.rebuilds == b.stats.rebuilds
-    out["graph_equals_eager"] = bool(ok)
-    out["graph_rebuilds"] = b.stats.rebuilds
-    out["graph_interactions_equal"] = a.interactions() == b.interactions()
-    gr.close()
+    # 2. captured multi-rank step == eager NCCL steps, bit for bit (two launches), with the
+    #    re-sort at every rebuild (momenta read from the share buffers) and with fixed ownership
+    for resort in (True, False):
+        a, b = sim(reorder=True), sim(reorder=True)    # both start with one re-sort
+        a.reorder = resort
+        n_steps = 30
+        gr = b.graph_collective(n_steps, resort=resort)
+        ok = True
+        for launch in range(2):
+            for _ in range(n_steps):
+                a.kick(w.dt, a.counter)
+                a.drift_and_exchange()
+            gr.launch()
+            torch.cuda.synchronize()
+            gr.finish()
+            ok = ok and torch.equal(a.q[:, :3], b.q[:, :3]) and torch.equal(a.p, b.p)
+            ok = ok and a.stats.rebuilds == b.stats.rebuilds
+        tag = "resort" if resort else "fixed"
+        out[f"graph_equals_eager_{tag}"] = bool(ok)
+        out[f"graph_rebuilds_{tag}"] = b.stats.rebuilds
+        out[f"graph_interactions_equal_{tag}"] = a.interactions() == b.interactions()
+        gr.close()
+        b.close()
 
     # 3. asynchronous all-gather + interior/boundary split == blocking exchange
     c, d = sim(overlap=False), sim(overlap=True)

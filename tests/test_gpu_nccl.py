@@ -50,10 +50,11 @@ def test_eager_nccl_steps_match_oracle(result):
     assert abs(ours - ref) <= 3
 
 
-def test_captured_multirank_step_equals_eager(result):
-    assert result["graph_rebuilds"] >= 3
-    assert result["graph_equals_eager"]
-    assert result["graph_interactions_equal"]
+@pytest.mark.parametrize("tag", ["resort", "fixed"])
+def test_captured_multirank_step_equals_eager(result, tag):
+    assert result[f"graph_rebuilds_{tag}"] >= 3
+    assert result[f"graph_equals_eager_{tag}"]
+    assert result[f"graph_interactions_equal_{tag}"]
 
 
 def test_async_allgather_overlap_equals_blocking(result):

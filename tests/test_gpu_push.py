@@ -158,3 +158,50 @@ def test_push_against_the_oracle(lj):
         assert np.array_equal(t[lo:hi, :3].cpu().numpy(), ref[lo:hi])
         assert not t[:lo].any() and not t[hi:].any()
     assert out.item() == oracle.max_displacement(ref, qrefn, b, e)
+
+
+@pytest.mark.parametrize("P", [1, 3, 4])
+def test_resort_with_peer_momenta_emulated_ranks(lj, P):
+    """lj_permute_rows_peers (the multi-rank re-sort of graph_collective) with P emulated
+    ranks on one GPU: rank k's share buffer holds only its own rows' momenta (the rest is
+    junk); for every rank r, perm is the oracle's cell order, q_out = q[perm], and the own
+    new rows of p_out are the global momenta of the permuted atoms, read from whichever
+    rank owned each atom -- other rows untouched."""
+    import lj_inputs
+    import oracle
+    w = lj_inputs.config(1)
+    n = w.n - w.n % P
+    qn = np.ascontiguousarray(w.q[:n])
+    n_own = n // P
+    g = lj.geom(w.L, w.rc, w.rs)
+    rng = np.random.default_rng(P)
+    pg = rng.normal(0, 1, (n, 3))
+    p_glob = lj.pack_aos4(torch.from_numpy(pg).cuda())
+    shares = []
+    for k in range(P):
+        s = torch.full((n, 4), -7.0, dtype=torch.float64, device="cuda")
+        s[k * n_own:(k + 1) * n_own] = p_glob[k * n_own:(k + 1) * n_own]
+        shares.append(s)
+    table = torch.tensor([s.data_ptr() for s in shares], dtype=torch.int64, device="cuda")
+    import ctypes
+    b = ctypes.c_size_t()
+    assert lj.load().lj_build_list_workspace(n, g, ctypes.byref(b)) == 0
+    ws = torch.empty(b.value, dtype=torch.uint8, device="cuda")
+    ref_perm = oracle.cell_order(qn, w.L, w.rs)
+    for r in range(P):
+        q = lj.pack_aos4(torch.from_numpy(qn).cuda())
+        q_out = torch.zeros_like(q)
+        q_ref = torch.zeros_like(q)
+        p_out = torch.full((n, 4), 5.0, dtype=torch.float64, device="cuda")
+        perm = torch.empty(n, dtype=torch.int64, device="cuda")
+        lj.permute_rows_peers(q, q_out, q_ref, p_out, table, n_own, r * n_own, (r + 1) * n_own, perm, g, ws)
+        torch.cuda.synchronize()
+        pm = perm.cpu().numpy()
+        assert np.array_equal(pm, ref_perm)
+        assert np.array_equal(q_out[:, :3].cpu().numpy(), oracle.wrap(qn, w.L)[pm])
+        assert torch.equal(q_ref, q_out)
+        own = slice(r * n_own, (r + 1) * n_own)
+        assert np.array_equal(p_out[own, :3].cpu().numpy(), pg[pm[own]])
+        rest = torch.ones(n, dtype=torch.bool, device="cuda")
+        rest[own] = False
+        assert bool((p_out[rest] == 5.0).all())
