@@ -650,8 +650,10 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config{args.config}", "n_atoms": w.n, "list": "half" if half else "full",
-                       "order": order + ((" (sorted once, then fixed row ownership)" if sim.collective and
-                                          md_graph is not None else " (re-sorted at every rebuild)")
+                       "order": order + ((" (re-sorted at every rebuild)" if sim.reorder else
+                                          " (sorted once, then fixed row ownership)")
+                                         + (", new own rows' momenta read from the owner ranks over NVLink"
+                                            if sim.reorder and sim.collective and md_graph is not None else "")
                                          if order == "cell" and not force_only else ""),
                        "dt": w.dt, "rc": w.rc, "rs": w.rs, "parallelism": f"rows/{world}",
                        "exchange": (("fused integrate + NVLink push" if sim.push else "halo" if sim.halo else "all-gather")
