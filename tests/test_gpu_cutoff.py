@@ -67,8 +67,7 @@ LANES = ([g | (u << 8) for g in (1, 2, 4, 8, 16, 32) for u in (2, 3, 4)] + [0]
          + [g | (v << 8) | IDXV for g in (1, 2, 4, 8, 16) for v in (2, 4)])
 
 
-@pytest.mark.parametrize("half", [False, True])
-@pytest.mark.parametrize("lanes", LANES)
+@pytest.mark.parametrize("half,lanes", [(h, x) for h in (False, True) for x in LANES])
 def test_force_at_cutoff_edge(lj, dev, star, half, lanes):
     g = lj.geom(L_STAR, 3.0, 3.3)
     q = to_dev(star["q"], dev)
