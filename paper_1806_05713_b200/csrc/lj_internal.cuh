@@ -39,7 +39,7 @@ struct CellGrid {
 // Workspace carve-out (offsets in bytes, 256-B aligned).
 struct BuildWorkspace {
     size_t off_cell_of, off_count, off_start, off_cursor, off_atoms, off_qcell, off_qf, off_qr, off_scan, off_over,
-        off_flags, off_ptrtmp, off_scratch, total;
+        off_flags, off_ptrtmp, off_scratch, off_setup, total;
     int64_t scan_blocks;
 };
 

@@ -300,6 +300,7 @@ struct ListArgs {
     double w;                 // cell width L / nc
     float lo2, hi2;           // fp32 decision band around rs2: r2f < lo2 accept, r2f >= hi2 reject
     float rb2;                // squared reach of a half-cell box (rounded-box candidate screen)
+    const struct CellSetup* setups;   // per-cell neighbour runs (k_cell_setup), v4 only
 };
 
 // Exact accept test on raw fp64 coordinates, bit-identical to the oracle's
@@ -629,6 +630,114 @@ __device__ __forceinline__ unsigned type_mask(const float4& f, float hw, float f
     return tm;
 }
 
+// The 27 neighbour runs of a cell in ascending cell id (= rank order): start,
+// count (as offsets), periodic offset, first / last atom index; whether the
+// storage is in cell order there; whether the cell holds own rows.  Computed for
+// every cell up front by k_cell_setup (one warp per cell, no barriers), and
+// copied into k_list_v4's shared memory with cp.async while the previous cell's
+// work items run -- so no warp of the builder waits for a serial setup warp.
+struct __align__(16) CellSetup {
+    int64_t start[27];
+    int off[28];
+    int first[27], last[27];
+    int any, unsorted;
+    signed char dc[27][3];   // neighbour cell offset (-1, 0, 1) per axis
+    signed char pad_[16 - (27 * 3) % 16];
+};
+static_assert(sizeof(CellSetup) % 16 == 0, "CellSetup is copied in 16-byte pieces");
+
+__device__ __forceinline__ void setup_cell(const ListArgs& a, int64_t c, CellSetup& S, int lane) {
+    const int nc = a.cg.nc;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t cs = a.start[c];
+    const int ccnt = (int)(a.start[c + 1] - cs);
+    const int ncz = (int)(c % nc), ncy = (int)((c / nc) % nc), ncx = (int)(c / ((int64_t)nc * nc));
+    int cnt = 0, rank = 31, first = 0, last = 0;
+    if (lane < 27) {
+        const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
+        int x = ncx + dx, y = ncy + dy, z = ncz + dz;
+        x += x < 0 ? nc : (x >= nc ? -nc : 0);
+        y += y < 0 ? nc : (y >= nc ? -nc : 0);
+        z += z < 0 ? nc : (z >= nc ? -nc : 0);
+        const int64_t cc = ((int64_t)x * nc + y) * nc + z;
+        const int64_t st = a.start[cc];
+        cnt = (int)(a.start[cc + 1] - st);
+        rank = axis_rank(ncx, dx, nc) * 9 + axis_rank(ncy, dy, nc) * 3 + axis_rank(ncz, dz, nc);
+        S.start[rank] = st;
+        S.dc[rank][0] = (signed char)dx;
+        S.dc[rank][1] = (signed char)dy;
+        S.dc[rank][2] = (signed char)dz;
+        if (cnt > 0) {
+            first = a.atoms[st];
+            last = a.atoms[st + cnt - 1];
+        }
+    }
+    bool mine = false;   // does this cell hold rows of [row_begin, row_end)?
+    for (int t = lane; t < ccnt; t += 32) {
+        const int i = a.atoms[cs + t];
+        mine |= i >= a.row_begin && i < a.row_end;
+    }
+    // in rank order: lane r handles the neighbour of rank r (lane `src` computed it)
+    int src = 0;
+#pragma unroll
+    for (int l = 0; l < 27; l++) src = (__shfl_sync(0xffffffffu, rank, l) == lane) ? l : src;
+    const int mycnt_r = __shfl_sync(0xffffffffu, cnt, src);
+    const int mycnt = lane < 27 ? mycnt_r : 0;
+    int incl = mycnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int rf = __shfl_sync(0xffffffffu, first, src);
+    const int rl = __shfl_sync(0xffffffffu, last, src);
+    if (lane < 27) S.off[lane + 1] = incl;
+    if (lane == 0) S.off[0] = 0;
+    // candidates already ascending (atoms stored in cell order)?  Each cell's atoms
+    // are ascending (k_cell_sort_gather), so only run boundaries can break the order.
+    const unsigned ne = __ballot_sync(0xffffffffu, mycnt > 0);
+    const unsigned before = ne & lt;
+    const int prev = before ? 31 - __clz(before) : 0;
+    const int prev_last = __shfl_sync(0xffffffffu, rl, prev);
+    const unsigned bad = __ballot_sync(0xffffffffu, mycnt > 0 && before != 0 && prev_last > rf);
+    const unsigned any = __ballot_sync(0xffffffffu, mine);
+    // how far from sorted: pairs of runs whose index intervals overlap (storage that has
+    // drifted from cell order since the last sort: a few migrants per cell, few overlaps;
+    // shuffled storage: nearly all 351 pairs overlap)
+    int ovl = 0;
+    if (bad) {
+        for (int u = 0; u < 27; u++) {
+            const int fu = __shfl_sync(0xffffffffu, rf, u), lu = __shfl_sync(0xffffffffu, rl, u);
+            const int cu = __shfl_sync(0xffffffffu, mycnt, u);
+            ovl += (lane < 27 && u > lane && mycnt > 0 && cu > 0 && !(lu < rf || fu > rl)) ? 1 : 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ovl += __shfl_xor_sync(0xffffffffu, ovl, o);
+    }
+    if (lane < 27) {
+        S.first[lane] = mycnt > 0 ? rf : INT_MAX;
+        S.last[lane] = mycnt > 0 ? rl : INT_MIN;
+    }
+    if (lane == 0) {
+        S.unsorted = bad == 0 ? 0 : (ovl <= kRankPathMaxOverlaps ? 1 : 2);
+        S.any = any != 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_cell_setup(ListArgs a, CellSetup* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < a.ncell;
+         c += ((int64_t)gridDim.x * blockDim.x) >> 5)
+        setup_cell(a, c, out[c], lane);
+}
+
+// 16-byte asynchronous copy global -> shared (LDGSTS): lands without registers.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int DIRECT, int HALF>
 __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
     if (a.flags[0]) return;   // unwrapped input: the exact kernel (k_list_v2) builds the list
@@ -644,11 +753,8 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
     float* CZ = CY + kCS;
     int* CJ = reinterpret_cast<int*>(CZ + kCS);
     unsigned char* TM = reinterpret_cast<unsigned char*>(CJ + kCS);
-    __shared__ int64_t s_start[27];
-    __shared__ int s_off[28];
-    __shared__ signed char s_dc[27][3];   // neighbour cell offset (-1, 0, 1) per axis
-    __shared__ int s_any, s_unsorted, s_next;
-    __shared__ int s_first[27], s_last[27];   // first / last atom index of each neighbour run (rank order)
+    __shared__ CellSetup s_set;   // this cell's neighbour runs (k_cell_setup), prefetched by cp.async
+    __shared__ int s_next;
     __shared__ int s_tlen[8];
     __shared__ float4 s_row[kMaxRows];
     __shared__ unsigned char s_rtau[kMaxRows], s_rk[kMaxRows], s_rowlist[kMaxRows];
@@ -661,95 +767,40 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
     const float hw = (float)(0.5 * a.w), fw = (float)a.w;
     const unsigned lt = (1u << lane) - 1u;
     constexpr int kTL = kMaxCand + 64;   // per-type list capacity
+    constexpr int kSetupChunks = (int)(sizeof(CellSetup) / 16);
+    static_assert(kSetupChunks <= kListWarps * 32, "one 16-byte chunk per thread");
+    if ((int64_t)blockIdx.x < a.ncell && tid < kSetupChunks)
+        cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid, reinterpret_cast<const char*>(a.setups + blockIdx.x) + 16 * tid);
+    if (tid < 8) s_rcnt[tid] = 0;   // (reset again during every cell's work items, where it is unused)
     for (int64_t c = blockIdx.x; c < a.ncell; c += gridDim.x) {
         const int64_t cs = a.start[c];
         const int ccnt = (int)(a.start[c + 1] - cs);
-        __syncthreads();   // smem of the previous cell no longer in use
-        if (w == 0) {
-            // the 27 neighbour cells in ascending cell id: runs and offsets
-            const int ncz = (int)(c % nc), ncy = (int)((c / nc) % nc), ncx = (int)(c / ((int64_t)nc * nc));
-            int cnt = 0, rank = 31, first = 0, last = 0;
-            if (lane < 27) {
-                const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
-                int x = ncx + dx, y = ncy + dy, z = ncz + dz;
-                x += x < 0 ? nc : (x >= nc ? -nc : 0);
-                y += y < 0 ? nc : (y >= nc ? -nc : 0);
-                z += z < 0 ? nc : (z >= nc ? -nc : 0);
-                const int64_t cc = ((int64_t)x * nc + y) * nc + z;
-                const int64_t st = a.start[cc];
-                cnt = (int)(a.start[cc + 1] - st);
-                rank = axis_rank(ncx, dx, nc) * 9 + axis_rank(ncy, dy, nc) * 3 + axis_rank(ncz, dz, nc);
-                s_start[rank] = st;
-                s_dc[rank][0] = (signed char)dx;
-                s_dc[rank][1] = (signed char)dy;
-                s_dc[rank][2] = (signed char)dz;
-                s_off[rank + 1] = cnt;
-                if (cnt > 0) {
-                    first = a.atoms[st];
-                    last = a.atoms[st + cnt - 1];
-                }
-            }
-            bool mine = false;   // does this cell hold rows of [row_begin, row_end)?
-            for (int t = lane; t < ccnt; t += 32) {
-                const int i = a.atoms[cs + t];
-                mine |= i >= a.row_begin && i < a.row_end;
-            }
-            __syncwarp();
-            // in rank order: lane r handles the neighbour of rank r
-            const int mycnt = lane < 27 ? s_off[lane + 1] : 0;
-            int incl = mycnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            // first/last atom of the run of rank `lane` (lane `src` computed it)
-            int src = 0;
-#pragma unroll
-            for (int l = 0; l < 27; l++) src = (__shfl_sync(0xffffffffu, rank, l) == lane) ? l : src;
-            const int rf = __shfl_sync(0xffffffffu, first, src);
-            const int rl = __shfl_sync(0xffffffffu, last, src);
-            __syncwarp();
-            if (lane < 27) s_off[lane + 1] = incl;
-            if (lane == 0) s_off[0] = 0;
-            // candidates already ascending (atoms stored in cell order)?  Each cell's atoms
-            // are ascending (k_cell_sort_gather), so only run boundaries can break the order.
-            const unsigned ne = __ballot_sync(0xffffffffu, mycnt > 0);
-            const unsigned before = ne & lt;
-            const int prev = before ? 31 - __clz(before) : 0;
-            const int prev_last = __shfl_sync(0xffffffffu, rl, prev);
-            const unsigned bad = __ballot_sync(0xffffffffu, mycnt > 0 && before != 0 && prev_last > rf);
-            const unsigned any = __ballot_sync(0xffffffffu, mine);
-            // how far from sorted: pairs of runs whose index intervals overlap (storage that has
-            // drifted from cell order since the last sort: a few migrants per cell, few overlaps;
-            // shuffled storage: nearly all 351 pairs overlap)
-            int ovl = 0;
-            for (int u = 0; u < 27; u++) {
-                const int fu = __shfl_sync(0xffffffffu, rf, u), lu = __shfl_sync(0xffffffffu, rl, u);
-                const int cu = __shfl_sync(0xffffffffu, mycnt, u);
-                ovl += (lane < 27 && u > lane && mycnt > 0 && cu > 0 && !(lu < rf || fu > rl)) ? 1 : 0;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ovl += __shfl_xor_sync(0xffffffffu, ovl, o);
-            if (lane < 27) {
-                s_first[lane] = mycnt > 0 ? rf : INT_MAX;
-                s_last[lane] = mycnt > 0 ? rl : INT_MIN;
-            }
-            if (lane == 0) {
-                s_unsorted = bad == 0 ? 0 : (ovl <= kRankPathMaxOverlaps ? 1 : 2);
-                s_any = any != 0;
-                s_next = 0;
-            }
-            if (lane < 8) s_rcnt[lane] = 0;
+        cp_async_wait_all();   // this cell's setup (issued during the previous cell's work items)
+        __syncthreads();   // smem of the previous cell no longer in use; this cell's setup visible
+        if (tid == 0) s_next = 0;   // (after the barrier: the previous cell's items are all taken)
+#define s_start s_set.start
+#define s_off s_set.off
+#define s_dc s_set.dc
+#define s_first s_set.first
+#define s_last s_set.last
+#define s_unsorted s_set.unsorted
+        if (!s_set.any) {
+            __syncthreads();   // everyone has read s_set before it is overwritten
+            if (c + gridDim.x < a.ncell && tid < kSetupChunks)
+                cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid,
+                           reinterpret_cast<const char*>(a.setups + c + gridDim.x) + 16 * tid);
+            continue;
         }
-        __syncthreads();
-        if (!s_any) continue;
         const int M = s_off[27];
         if (M > kMaxCand || ccnt > kMaxRows) {
             if (!DIRECT && tid == 0) {
                 int k = atomicAdd(&a.n_overflow[0], 1);
                 a.overflow_cells[k] = (int)c;
             }
+            __syncthreads();   // everyone has read s_set before it is overwritten
+            if (c + gridDim.x < a.ncell && tid < kSetupChunks)
+                cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid,
+                           reinterpret_cast<const char*>(a.setups + c + gridDim.x) + 16 * tid);
             continue;
         }
         const int M32 = (M + 31) & ~31;
@@ -908,6 +959,12 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
             if (tau == 7 && lane == 0) s_nitems = ibase + k;
         }
         __syncthreads();
+        // s_set and s_rcnt are no longer read in this cell: fetch the next cell's setup behind the
+        // work items and clear the row counts for the next cell's rows phase
+        if (tid < 8) s_rcnt[tid] = 0;
+        if (c + gridDim.x < a.ncell && tid < kSetupChunks)
+            cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid,
+                       reinterpret_cast<const char*>(a.setups + c + gridDim.x) + 16 * tid);
         // work items: rows of one type (in registers) against the type's candidate list
         for (;;) {
             int it = 0;
@@ -975,6 +1032,13 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
         }
     }
 }
+
+#undef s_start
+#undef s_off
+#undef s_dc
+#undef s_first
+#undef s_last
+#undef s_unsorted
 
 // Fallback for cells with more than kMaxCand candidates (dense or tiny boxes):
 // one warp per row straight from global memory, per-row bitonic sort.
@@ -1187,6 +1251,8 @@ BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows) {
     o = align256(o + sizeof(int64_t) * (size_t)(rows + 1));
     W.off_scratch = o; // rows * kRowCap int32
     o = align256(o + sizeof(int32_t) * (size_t)rows * kRowCap);
+    W.off_setup = o;   // ncell CellSetup records (k_cell_setup -> k_list_v4)
+    o = align256(o + sizeof(CellSetup) * (size_t)ncell);
     W.total = o;
     return W;
 }
@@ -1309,6 +1375,7 @@ static ListArgs list_args(const double* q, const CellGrid& cg, double rs, int ha
     a.out = out;
     a.n_overflow = (int32_t*)(ws + W.off_over);
     a.overflow_cells = a.n_overflow + 2;
+    a.setups = (const CellSetup*)(ws + W.off_setup);
     a.clamp = 0;
     return a;
 }
@@ -1349,6 +1416,8 @@ static cudaError_t set_list_attrs() {
 // returns at once unless the input-range flag of k_cell_assign selects it.
 template <int DIRECT>
 static void launch_list_kernels(const ListArgs& a, const CellGrid& cg, int half, cudaStream_t s) {
+    k_cell_setup<<<grid_for(cg.ncell * 32, 256, 148 * 16), 256, 0, s>>>(a, const_cast<CellSetup*>(a.setups));
+    g_launches++;
     if (half) {
         k_list_v4<DIRECT, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmemV4, s>>>(a);
         k_list_v2<DIRECT, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
