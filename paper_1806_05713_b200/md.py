@@ -614,7 +614,12 @@ class LeapfrogMD:
                 self.p_alt = self.be.empty_records(self.n)
             if getattr(self.be, "perm", None) is None:
                 self.be.perm = torch.empty(self.n, dtype=torch.int64, device=self.q.device)
-            self._p_share, self._p_tables = self._open_momentum_shares()
+            if self.world > 1:
+                self._p_share, self._p_tables = self._open_momentum_shares()
+            else:   # one rank: the momenta are read from p itself (no copy, no peers)
+                self._p_share = None
+                t = torch.tensor([self.p.data_ptr()], dtype=torch.int64, device=self.q.device)
+                self._p_tables = [t, t]
             rs = [dict(q_alt=self.q_alt, p=self.p, p_alt=self.p_alt, perm=self.be.perm, p_peers=self._p_tables[b],
                        n_own=n_own) for b in range(2)]
         g = torch.cuda.CUDAGraph()
@@ -626,7 +631,7 @@ class LeapfrogMD:
             for k in range(steps):
                 self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
                 self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, self.rb, self.re, self.disp)
-                if resort:
+                if resort and self._p_share is not None:
                     lj.copy_records(self.p[self.rb:self.re], self._p_share[k % 2][self.rb:self.re])
                 lj.publish_scalar(self.disp, own_pad)
                 dist.all_gather_into_tensor(self.q, self.q[self.rb:self.re], group=self.comm)
