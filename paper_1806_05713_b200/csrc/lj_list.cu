@@ -289,8 +289,9 @@ struct ListArgs {
     int32_t* npart;           // [rows]
     const int64_t* ptr;       // [rows+1] (direct mode)
     int32_t* out;             // scratch [rows * kRowCap] or list
-    int32_t* overflow_cells;  // cells with more than kMaxCand candidates
-    int32_t* n_overflow;      // [0] = #overflow cells, [1] = row overflow flag
+    int32_t* overflow_cells;  // cells the first pass could not stage (-> the LARGE pass)
+    int32_t* overflow_cells2; // cells the LARGE pass could not stage either, and the exact kernel's (-> fallback)
+    int32_t* n_overflow;      // [0] = #overflow_cells, [1] = row overflow flag, [2] = #overflow_cells2
     int clamp;                // out is the caller's padded list: a row over kRowCap stores
                               // min(count, kRowCap) in npart (consumers stay in bounds until
                               // the overflow flag is seen); scratch mode keeps the true count
@@ -387,9 +388,9 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
         if (!s_any) continue;
         const int M = s_off[27];
         if (M > kMaxCand) {
-            if (!DIRECT && tid == 0) {
-                int k = atomicAdd(&a.n_overflow[0], 1);
-                a.overflow_cells[k] = (int)c;
+            if (!DIRECT && tid == 0) {   // (the LARGE v4 pass does not run on unwrapped input)
+                int k = atomicAdd(&a.n_overflow[2], 1);
+                a.overflow_cells2[k] = (int)c;
             }
             continue;
         }
@@ -738,17 +739,21 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int DIRECT, int HALF>
-__global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
+// MAXC: candidates staged per cell (MAXC = 1344 for 4 CTAs/SM; the LARGE instantiation,
+// MAXCLarge, takes the cells the first pass could not stage -- small or dense boxes, e.g.
+// config 1's 1,687 candidates per cell -- from its overflow list; what it cannot stage either
+// goes to k_list_fallback).
+template <int DIRECT, int HALF, int MAXC, bool LARGE>
+__global__ void __launch_bounds__(kListWarps * 32, LARGE ? 2 : 4) k_list_v4(ListArgs a) {
     if (a.flags[0]) return;   // unwrapped input: the exact kernel (k_list_v2) builds the list
     extern __shared__ __align__(16) unsigned char smem[];
-    unsigned short* tl = reinterpret_cast<unsigned short*>(smem);            // [8][kMaxCand + 64] slot lists
+    unsigned short* tl = reinterpret_cast<unsigned short*>(smem);            // [8][MAXC + 64] slot lists
     unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);   // (aliased) unsorted staging only
     // staged candidates, structure of arrays (x, y, z, atom index) so that the two
     // candidates a lane tests load straight into an fp32x2 register pair;
-    // slot kMaxCand is the sentinel
-    constexpr int kCS = kMaxCand + 32;
-    float* CX = reinterpret_cast<float*>(smem + 8 * (kMaxCand + 64) * 2);
+    // slot MAXC is the sentinel
+    constexpr int kCS = MAXC + 32;
+    float* CX = reinterpret_cast<float*>(smem + 8 * (MAXC + 64) * 2);
     float* CY = CX + kCS;
     float* CZ = CY + kCS;
     int* CJ = reinterpret_cast<int*>(CZ + kCS);
@@ -766,13 +771,21 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
     const double L = a.cg.L, halfL = 0.5 * a.cg.L;
     const float hw = (float)(0.5 * a.w), fw = (float)a.w;
     const unsigned lt = (1u << lane) - 1u;
-    constexpr int kTL = kMaxCand + 64;   // per-type list capacity
+    constexpr int kTL = MAXC + 64;   // per-type list capacity
     constexpr int kSetupChunks = (int)(sizeof(CellSetup) / 16);
     static_assert(kSetupChunks <= kListWarps * 32, "one 16-byte chunk per thread");
-    if ((int64_t)blockIdx.x < a.ncell && tid < kSetupChunks)
-        cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid, reinterpret_cast<const char*>(a.setups + blockIdx.x) + 16 * tid);
+    // the cells this kernel visits: all (first pass) or the first pass's overflow list (LARGE)
+    const int64_t n_visit = LARGE ? (int64_t)a.n_overflow[0] : a.ncell;
+    auto cell_at = [&](int64_t k) -> int64_t { return LARGE ? (int64_t)a.overflow_cells[k] : k; };
+    auto prefetch = [&](int64_t k) {   // the setup of the k-th visited cell into s_set (cp.async)
+        if (k < n_visit && tid < kSetupChunks)
+            cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid,
+                       reinterpret_cast<const char*>(a.setups + cell_at(k)) + 16 * tid);
+    };
+    prefetch(blockIdx.x);
     if (tid < 8) s_rcnt[tid] = 0;   // (reset again during every cell's work items, where it is unused)
-    for (int64_t c = blockIdx.x; c < a.ncell; c += gridDim.x) {
+    for (int64_t kv = blockIdx.x; kv < n_visit; kv += gridDim.x) {
+        const int64_t c = cell_at(kv);
         const int64_t cs = a.start[c];
         const int ccnt = (int)(a.start[c + 1] - cs);
         cp_async_wait_all();   // this cell's setup (issued during the previous cell's work items)
@@ -786,21 +799,17 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
 #define s_unsorted s_set.unsorted
         if (!s_set.any) {
             __syncthreads();   // everyone has read s_set before it is overwritten
-            if (c + gridDim.x < a.ncell && tid < kSetupChunks)
-                cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid,
-                           reinterpret_cast<const char*>(a.setups + c + gridDim.x) + 16 * tid);
+            prefetch(kv + gridDim.x);
             continue;
         }
         const int M = s_off[27];
-        if (M > kMaxCand || ccnt > kMaxRows) {
-            if (!DIRECT && tid == 0) {
-                int k = atomicAdd(&a.n_overflow[0], 1);
-                a.overflow_cells[k] = (int)c;
+        if (M > MAXC || ccnt > kMaxRows) {
+            if (!DIRECT && tid == 0) {   // first pass: to the LARGE pass; LARGE: to the fallback
+                const int k = atomicAdd(&a.n_overflow[LARGE ? 2 : 0], 1);
+                (LARGE ? a.overflow_cells2 : a.overflow_cells)[k] = (int)c;
             }
             __syncthreads();   // everyone has read s_set before it is overwritten
-            if (c + gridDim.x < a.ncell && tid < kSetupChunks)
-                cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid,
-                           reinterpret_cast<const char*>(a.setups + c + gridDim.x) + 16 * tid);
+            prefetch(kv + gridDim.x);
             continue;
         }
         const int M32 = (M + 31) & ~31;
@@ -909,8 +918,8 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
         }
         for (int s = M + tid; s < M32; s += blockDim.x) TM[s] = 0;
         if (tid == 0) {   // sentinel
-            CX[kMaxCand] = CY[kMaxCand] = CZ[kMaxCand] = 1e30f;
-            CJ[kMaxCand] = -1;
+            CX[MAXC] = CY[MAXC] = CZ[MAXC] = 1e30f;
+            CJ[MAXC] = -1;
         }
         // rows of this cell and their half-cell types
         for (int t = tid; t < ccnt; t += blockDim.x) {
@@ -936,7 +945,7 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
                 n += __popc(m);
             }
             const int padded = (n + 63) & ~63;
-            for (int k = n + lane; k < padded; k += 32) lst[k] = (unsigned short)kMaxCand;
+            for (int k = n + lane; k < padded; k += 32) lst[k] = (unsigned short)MAXC;
             if (lane == 0) s_tlen[tau] = padded;
             int rbase = 0, ibase = 0;
 #pragma unroll
@@ -962,9 +971,7 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v4(ListArgs a) {
         // s_set and s_rcnt are no longer read in this cell: fetch the next cell's setup behind the
         // work items and clear the row counts for the next cell's rows phase
         if (tid < 8) s_rcnt[tid] = 0;
-        if (c + gridDim.x < a.ncell && tid < kSetupChunks)
-            cp_async16(reinterpret_cast<char*>(&s_set) + 16 * tid,
-                       reinterpret_cast<const char*>(a.setups + c + gridDim.x) + 16 * tid);
+        prefetch(kv + gridDim.x);
         // work items: rows of one type (in registers) against the type's candidate list
         for (;;) {
             int it = 0;
@@ -1047,9 +1054,9 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_fallback(ListArgs a) {
     __shared__ int rowbuf[kListWarps][kRowBuf];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const double L = a.cg.L, halfL = 0.5 * a.cg.L;
-    const int nover = a.n_overflow[0];
+    const int nover = a.n_overflow[2];
     for (int oc = blockIdx.x; oc < nover; oc += gridDim.x) {
-        const int c = a.overflow_cells[oc];
+        const int c = a.overflow_cells2[oc];
         const int64_t cs = a.start[c];
         const int ccnt = (int)(a.start[c + 1] - cs);
         for (int t = w; t < ccnt; t += kListWarps) {
@@ -1243,8 +1250,8 @@ BuildWorkspace build_workspace_layout(int64_t n, int64_t ncell, int64_t rows) {
     o = align256(o + sizeof(float4) * (size_t)n);
     W.off_scan = o;
     o = align256(o + sizeof(int64_t) * (size_t)(W.scan_blocks + 1));
-    W.off_over = o;    // [0] overflow cell count, [1] row overflow flag, then ncell cell ids
-    o = align256(o + sizeof(int32_t) * (size_t)(ncell + 2));
+    W.off_over = o;    // [0] / [2] overflow cell counts, [1] row overflow flag, [3] pad, then 2 x ncell cell ids
+    o = align256(o + sizeof(int32_t) * (size_t)(2 * ncell + 4));
     W.off_flags = o;   // [0] some raw coordinate outside [0, L) (set by k_cell_assign)
     o = align256(o + sizeof(int32_t) * 4);
     W.off_ptrtmp = o;  // rows + 1 int64 (padded layout: scan of the counts)
@@ -1329,6 +1336,8 @@ cudaError_t launch_rebuild_cells(double* q, const double* p, double* q_out, doub
     return cudaGetLastError();
 }
 
+static int64_t ncell_of(const CellGrid& cg) { return cg.ncell; }
+
 static ListArgs list_args(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
                           int64_t row_end, int32_t* npart, const int64_t* ptr, int32_t* out, char* ws,
                           const BuildWorkspace& W) {
@@ -1374,7 +1383,8 @@ static ListArgs list_args(const double* q, const CellGrid& cg, double rs, int ha
     a.ptr = ptr;
     a.out = out;
     a.n_overflow = (int32_t*)(ws + W.off_over);
-    a.overflow_cells = a.n_overflow + 2;
+    a.overflow_cells = a.n_overflow + 4;
+    a.overflow_cells2 = a.overflow_cells + ncell_of(cg);
     a.setups = (const CellSetup*)(ws + W.off_setup);
     a.clamp = 0;
     return a;
@@ -1386,7 +1396,10 @@ static int list_grid(const CellGrid& cg, int per_sm) {
 }
 
 constexpr size_t kListSmem = (size_t)kMaxCand * 8 + (size_t)(kMaxCand + 32) * (3 * 8 + 4 + 1);
-constexpr size_t kListSmemV4 = (size_t)8 * (kMaxCand + 64) * 2 + (size_t)(kMaxCand + 32) * (16 + 1);
+constexpr size_t list_smem_v4(int maxc) { return (size_t)8 * (maxc + 64) * 2 + (size_t)(maxc + 32) * (16 + 1); }
+constexpr int kMaxCandLarge = 2560;   // the LARGE pass: 2 CTAs per SM (86 KB of shared memory)
+constexpr size_t kListSmemV4 = list_smem_v4(kMaxCand);
+constexpr size_t kListSmemV4L = list_smem_v4(kMaxCandLarge);
 
 static cudaError_t set_list_attrs() {
     // cudaFuncSetAttribute is per device: one flag per device ordinal (set once, thread-safe)
@@ -1402,9 +1415,16 @@ static cudaError_t set_list_attrs() {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmem);
             if (e != cudaSuccess) return e;
         }
-        void (*fns4[4])(ListArgs) = {k_list_v4<0, 0>, k_list_v4<0, 1>, k_list_v4<1, 0>, k_list_v4<1, 1>};
+        void (*fns4[4])(ListArgs) = {k_list_v4<0, 0, kMaxCand, false>, k_list_v4<0, 1, kMaxCand, false>,
+                                     k_list_v4<1, 0, kMaxCand, false>, k_list_v4<1, 1, kMaxCand, false>};
         for (auto f : fns4) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmemV4);
+            if (e != cudaSuccess) return e;
+        }
+        void (*fns4l[4])(ListArgs) = {k_list_v4<0, 0, kMaxCandLarge, true>, k_list_v4<0, 1, kMaxCandLarge, true>,
+                                      k_list_v4<1, 0, kMaxCandLarge, true>, k_list_v4<1, 1, kMaxCandLarge, true>};
+        for (auto f : fns4l) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kListSmemV4L);
             if (e != cudaSuccess) return e;
         }
         done[dev].store(true, std::memory_order_release);   // idempotent: a race sets the same attributes twice
@@ -1419,14 +1439,16 @@ static void launch_list_kernels(const ListArgs& a, const CellGrid& cg, int half,
     k_cell_setup<<<grid_for(cg.ncell * 32, 256, 148 * 16), 256, 0, s>>>(a, const_cast<CellSetup*>(a.setups));
     g_launches++;
     if (half) {
-        k_list_v4<DIRECT, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmemV4, s>>>(a);
+        k_list_v4<DIRECT, 1, kMaxCand, false><<<list_grid(cg, 4), kListWarps * 32, kListSmemV4, s>>>(a);
+        k_list_v4<DIRECT, 1, kMaxCandLarge, true><<<list_grid(cg, 2), kListWarps * 32, kListSmemV4L, s>>>(a);
         k_list_v2<DIRECT, 1><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
     } else {
-        k_list_v4<DIRECT, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmemV4, s>>>(a);
+        k_list_v4<DIRECT, 0, kMaxCand, false><<<list_grid(cg, 4), kListWarps * 32, kListSmemV4, s>>>(a);
+        k_list_v4<DIRECT, 0, kMaxCandLarge, true><<<list_grid(cg, 2), kListWarps * 32, kListSmemV4L, s>>>(a);
         k_list_v2<DIRECT, 0><<<list_grid(cg, 4), kListWarps * 32, kListSmem, s>>>(a);
     }
     k_list_fallback<DIRECT><<<148, kListWarps * 32, 0, s>>>(a);
-    g_launches += 3;
+    g_launches += 4;
 }
 
 cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
@@ -1437,7 +1459,7 @@ cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, in
     ListArgs a = list_args(q, cg, rs, half, row_begin, row_end, npart, nullptr,
                            out ? out : (int32_t*)(ws + W.off_scratch), ws, W);
     a.clamp = out != nullptr;   // the caller's padded list: counts clamped to the stride
-    e = cudaMemsetAsync(a.n_overflow, 0, 2 * sizeof(int32_t), s);
+    e = cudaMemsetAsync(a.n_overflow, 0, 4 * sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     launch_list_kernels<0>(a, cg, half, s);
     return cudaGetLastError();
