@@ -9,6 +9,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblj.so")
+# the memory-safety build: the same sources with -DLJ_CHECK (device-side bounds checks that
+# trap; tests/test_gpu_checked.py runs parity tests against it via LJ_LIBRARY=check)
+LIB_CHECK = os.path.join(HERE, "liblj_check.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -27,29 +30,33 @@ def headers():
     return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(HERE, "..", "include", "*.h")))
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, *os.environ.get("NVCC_EXTRA", "").split(), "-o", tmp, *sources()]
+def build(force: bool = False, verbose: bool = False, check: bool = False) -> str:
+    """Build liblj.so (check=True: liblj_check.so with the LJ_CHECK bounds checks)."""
+    lib = LIB_CHECK if check else LIB
+    if not force and up_to_date(lib):
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    extra = ["-DLJ_CHECK"] if check else []
+    cmd = [NVCC, *NVCC_FLAGS, *extra, *os.environ.get("NVCC_EXTRA", "").split(), "-o", tmp, *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building liblj.so")
-    with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+        raise RuntimeError(f"nvcc failed building {os.path.basename(lib)}")
+    if not check:
+        with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
+            f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, check="--check" in sys.argv))

@@ -315,6 +315,7 @@ lj_status lj_force_step_ex(const double* q, double* p, int64_t n, lj_geom g, dou
     lanes |= unroll << 8 | idxv;
     ForceArgs a;
     a.q = q;
+    a.n = n;
     a.p = p;
     a.row_begin = row_begin;
     a.rows = rows;
@@ -371,6 +372,7 @@ lj_status lj_force_step_half_cells(const double* q, double* p, int64_t n, lj_geo
         return fail(LJ_ERR_ARG, "force_half_cells: lanes_per_row must be 0, 2|2<<8, 4|2<<8, 8|2<<8 or 4|3<<8");
     ForceArgs a;
     a.q = q;
+    a.n = n;
     a.p = p;
     a.row_begin = 0;
     a.rows = n;
@@ -405,6 +407,7 @@ lj_status lj_force_step_variant(int layout, int rcp, const double* q, double* p,
         return fail(LJ_ERR_ARG, "variant: q/p misaligned for the layout");
     ForceArgs a;
     a.q = q;
+    a.n = n;
     a.p = p;
     a.row_begin = row_begin;
     a.rows = rows;
@@ -433,6 +436,7 @@ lj_status lj_gather_probe(const double* q, int64_t n, int64_t row_begin, int64_t
     if (((lanes >> 8) & 0xff) == 0) lanes |= 2 << 8;
     ForceArgs a;
     a.q = q;
+    a.n = n;
     a.p = nullptr;
     a.row_begin = row_begin;
     a.rows = row_end - row_begin;
@@ -620,6 +624,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
     LJ_G(cudaGraphCreate(&gr->graph, 0), "md_graph/create");
     ForceArgs fa;
     fa.q = d->q;
+    fa.n = n;
     fa.p = d->p;
     fa.row_begin = 0;
     fa.rows = n;
@@ -651,7 +656,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
             half_kick.dt = 0.5 * d->dt;
             e = launch_force_full(half_kick, lanes, cs);
             if (e == cudaSuccess)
-                e = launch_energy(d->q, d->p, 0, n, d->number_of_partners, d->pointer, d->sorted_list, d->g.L,
+                e = launch_energy(d->q, d->p, n, 0, n, d->number_of_partners, d->pointer, d->sorted_list, d->g.L,
                                   d->g.rc * d->g.rc, d->g.rc, 0, d->energies + 2 * (k / d->energy_every), cs);
             half_kick.n_inter = nullptr;
             if (e == cudaSuccess) e = launch_force_full(half_kick, lanes, cs);
@@ -914,7 +919,7 @@ lj_status lj_energy(const double* q, const double* p, int64_t n, lj_geom g, int6
     if (row_end > row_begin && (!q || !p || !number_of_partners || !pointer))
         return fail(LJ_ERR_ARG, "energy: null pointer");
     if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "energy: not 32-byte aligned");
-    LJ_CUDA(launch_energy(q, p, row_begin, row_end - row_begin, number_of_partners, pointer, sorted_list, g.L,
+    LJ_CUDA(launch_energy(q, p, n, row_begin, row_end - row_begin, number_of_partners, pointer, sorted_list, g.L,
                           g.rc * g.rc, g.rc, half, out, (cudaStream_t)stream),
             "lj_energy");
     return LJ_OK;

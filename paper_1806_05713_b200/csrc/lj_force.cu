@@ -38,6 +38,7 @@ struct PairConsts {
     double L;        // box side (0 = open)
     double c48, c24; // 48 dt, 24 dt
     double rc2;      // r_c^2 = rc*rc (the oracle's constant)
+    int64_t n_atoms; // (bounds checks of the LJ_CHECK build)
     long long rc2_bits;
     int rc2_hi;      // high word of rc2's IEEE bits
     int hi_halfL;    // high word of L/2 (INT_MAX for open boundaries)
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
 #pragma unroll
         for (int u = 0; u < U; u++) {
             j[u] = jn[u];
+            LJ_CHECK_THAT(j[u] < c.n_atoms);
             qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);   // no entry: r = 0, masked below
         }
 #pragma unroll
@@ -284,6 +286,7 @@ __global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
 #pragma unroll
         for (int u = 0; u < V; u++) {
             j[u] = (s0 + u >= off && s0 + u < end) ? jn[u] : -1;
+            LJ_CHECK_THAT(j[u] < c.n_atoms);
             qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);   // no entry: r = 0, masked below
         }
         const int sn = s0 + V * G;
@@ -498,6 +501,7 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     j[u] = jn[u];
+                    LJ_CHECK_THAT(j[u] < c.n_atoms);
                     qj[u] = load_rec(q, j[u] >= 0 ? (int64_t)j[u] : i);
                 }
 #pragma unroll
@@ -651,6 +655,7 @@ __global__ void __launch_bounds__(kForceThreads, (LAYOUT == LJ_LAYOUT_SOA || LAY
 #pragma unroll
         for (int u = 0; u < U; u++) {
             j[u] = jn[u];
+            LJ_CHECK_THAT(j[u] < n_atoms);
             Lay::pos(q, n_atoms, j[u] >= 0 ? (int64_t)j[u] : i, dx[u], dy[u], dz[u]);
         }
 #pragma unroll
@@ -801,7 +806,8 @@ __device__ __forceinline__ double min_image_exact(double d, double L) {
 __global__ void __launch_bounds__(kForceThreads)
     k_force_ordered(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
                     const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr,
-                    const int32_t* __restrict__ list, double L, double rc2, double dt, unsigned long long* n_inter) {
+                    const int32_t* __restrict__ list, double L, double rc2, double dt, unsigned long long* n_inter,
+                    int64_t n_atoms) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     unsigned cnt = 0;
     if (r < rows) {
@@ -811,6 +817,7 @@ __global__ void __launch_bounds__(kForceThreads)
         const int64_t beg = ptr[r];
         const int n = npart[r];
         for (int k = 0; k < n; k++) {
+            LJ_CHECK_THAT(list[beg + k] >= 0 && list[beg + k] < n_atoms);
             const rec4 qj = load_rec(q, list[beg + k]);
             double dx = min_image_exact(__dsub_rn(qj.x, qi.x), L);
             double dy = min_image_exact(__dsub_rn(qj.y, qi.y), L);
@@ -845,6 +852,7 @@ PairConsts make_consts(const ForceArgs& a) {
     c.rc2_bits = u.b;
     c.rc2_hi = (int)(u.b >> 32);
     c.rc2 = a.rc2;
+    c.n_atoms = a.n;
     if (a.L > 0.0) {
         u.d = 0.5 * a.L;
         c.hi_halfL = (int)(u.b >> 32);
@@ -1031,7 +1039,7 @@ cudaError_t launch_force_ordered(const ForceArgs& a, cudaStream_t s) {
     if (a.rows <= 0) return cudaSuccess;
     unsigned grid = (unsigned)((a.rows + kForceThreads - 1) / kForceThreads);
     k_force_ordered<<<grid, kForceThreads, 0, s>>>((const rec4*)a.q, (rec4*)a.p, a.row_begin, a.rows, a.npart, a.ptr,
-                                                   a.list, a.L, a.rc2, a.dt, a.n_inter);
+                                                   a.list, a.L, a.rc2, a.dt, a.n_inter, a.n);
     g_launches++;
     return cudaGetLastError();
 }

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdio>
 
 #include "../../include/liblj.h"
 
@@ -19,6 +20,24 @@ struct __align__(32) rec4 {
 };
 
 extern std::atomic<long long> g_launches;
+
+// Bounds checks of the memory-safety build (liblj_check.so, -DLJ_CHECK; tests/test_gpu_checked.py):
+// a violated condition prints where and traps, which surfaces as a CUDA error at the next
+// synchronising call.  Compiled out of liblj.so.
+#ifdef LJ_CHECK
+#define LJ_CHECK_THAT(cond)                                                                            \
+    do {                                                                                               \
+        if (!(cond)) {                                                                                 \
+            printf("liblj check failed: %s (%s:%d, block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                 \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#else
+#define LJ_CHECK_THAT(cond) \
+    do {                    \
+    } while (0)
+#endif
 
 // 256-bit read-only load of one record (compiles to LDG.E.ENL2.256.CONSTANT).
 __device__ __forceinline__ rec4 load_rec(const rec4* __restrict__ a, int64_t i) {
@@ -80,6 +99,7 @@ cudaError_t launch_permute(const double* in, double* out, const int64_t* perm, i
 struct ForceArgs {
     const double* q;
     double* p;
+    int64_t n;   // atoms (the range every list index must lie in)
     int64_t row_begin, rows;
     const int32_t* npart;
     const int64_t* ptr;
@@ -113,7 +133,8 @@ cudaError_t launch_partner_ranges(int64_t row_begin, int64_t row_end, const int3
                                   const int32_t* list, const int64_t* bounds, int P, int64_t* out, cudaStream_t s);
 cudaError_t launch_list_interior(int64_t row_begin, int64_t row_end, const int32_t* npart, const int64_t* ptr,
                                  const int32_t* list, int64_t* out, cudaStream_t s);
-cudaError_t launch_energy(const double* q, const double* p, int64_t row_begin, int64_t rows, const int32_t* npart,
+cudaError_t launch_energy(const double* q, const double* p, int64_t n, int64_t row_begin, int64_t rows,
+                          const int32_t* npart,
                           const int64_t* ptr, const int32_t* list, double L, double rc2, double rc, int half,
                           double* out, cudaStream_t s);
 

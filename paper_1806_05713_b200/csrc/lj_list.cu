@@ -980,6 +980,7 @@ __global__ void __launch_bounds__(kListWarps * 32, LARGE ? 2 : 4) k_list_v4(List
             if (it >= s_nitems) break;
             const int code = s_item[it];
             const int tau = code & 0xff, u0 = (code >> 8) & 0xff, nr = code >> 16;
+            LJ_CHECK_THAT(tau < 8 && nr <= kItemRows && u0 + nr <= ccnt);
             float4 ri[kItemRows];
             int32_t* dst[kItemRows];
             int cur[kItemRows];
@@ -998,6 +999,7 @@ __global__ void __launch_bounds__(kListWarps * 32, LARGE ? 2 : 4) k_list_v4(List
             const int len = s_tlen[tau];
             for (int k0 = 0; k0 < len; k0 += 64) {
                 const int s0 = lst[k0 + lane], s1 = lst[k0 + 32 + lane];
+                LJ_CHECK_THAT(s0 <= MAXC && s1 <= MAXC);
                 const int j0 = CJ[s0], j1 = CJ[s1];
                 // the two candidates side by side in packed fp32x2 registers (FADD2/FFMA2,
                 // row coordinate broadcast): same IEEE operations as the scalar form
@@ -1026,6 +1028,13 @@ __global__ void __launch_bounds__(kListWarps * 32, LARGE ? 2 : 4) k_list_v4(List
                     cur[r] += __popc(m0) + __popc(m1);
                 }
             }
+#ifdef LJ_CHECK
+            if (DIRECT) {   // the fill pass accepts exactly the count pass's entries
+#pragma unroll
+                for (int r = 0; r < kItemRows; r++)
+                    if (r < nr && lane == r) LJ_CHECK_THAT(cur[r] == a.npart[__float_as_int(ri[r].w) - a.row_begin]);
+            }
+#endif
             if (!DIRECT) {
 #pragma unroll
                 for (int r = 0; r < kItemRows; r++) {
@@ -1084,6 +1093,7 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_fallback(ListArgs a) {
                     const int pos = cursor + __popc(m & ((1u << lane) - 1u));
                     if (acc) {
                         if (pos < kRowBuf) buf[pos] = j;
+                        LJ_CHECK_THAT(!DIRECT || pos < a.npart[r]);
                         if (DIRECT) gdst[pos] = j;
                     }
                     cursor += __popc(m);

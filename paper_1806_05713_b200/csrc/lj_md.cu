@@ -190,7 +190,7 @@ __global__ void k_build_status(const int64_t* __restrict__ total, const int32_t*
 // minimum image as the oracle's branches; per-lane sums reduced per block.
 constexpr int kEnergyLanes = 8;
 __global__ void __launch_bounds__(kThreads)
-    k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p, int64_t row_begin, int64_t rows,
+    k_energy(const rec4* __restrict__ q, const rec4* __restrict__ p, int64_t n_atoms, int64_t row_begin, int64_t rows,
              const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
              double L, double rc2, double vc, int half, double* out) {
     constexpr int G = kEnergyLanes;
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kThreads)
         const int32_t* __restrict__ l = list + ptr[r];
         const int n = npart[r];
         for (int k = g; k < n; k += G) {
+            LJ_CHECK_THAT(l[k] >= 0 && l[k] < n_atoms);
             const rec4 qj = load_rec(q, __ldg(l + k));
             double dx = qj.x - qi.x, dy = qj.y - qi.y, dz = qj.z - qi.z;
             if (L > 0.0) {
@@ -440,7 +441,8 @@ cudaError_t launch_max_disp(const double* q, const double* q_ref, int64_t begin,
     return cudaGetLastError();
 }
 
-cudaError_t launch_energy(const double* q, const double* p, int64_t row_begin, int64_t rows, const int32_t* npart,
+cudaError_t launch_energy(const double* q, const double* p, int64_t n, int64_t row_begin, int64_t rows,
+                          const int32_t* npart,
                           const int64_t* ptr, const int32_t* list, double L, double rc2, double rc, int half,
                           double* out, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), s);
@@ -448,7 +450,7 @@ cudaError_t launch_energy(const double* q, const double* p, int64_t row_begin, i
     double rc6 = rc2 * rc2 * rc2;
     double vc = 4.0 * (1.0 / (rc6 * rc6) - 1.0 / rc6);
     k_energy<<<grid_for(rows * kEnergyLanes, kThreads, 148 * 8), kThreads, 0, s>>>(
-        (const rec4*)q, (const rec4*)p, row_begin, rows, npart, ptr, list, L, rc2, vc, half, out);
+        (const rec4*)q, (const rec4*)p, n, row_begin, rows, npart, ptr, list, L, rc2, vc, half, out);
     g_launches++;
     return cudaGetLastError();
 }

@@ -93,9 +93,13 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"liblj.so not built ({LIB_PATH}); run python -c 'import __graft_entry__ as g; g.build()'")
-    L = ctypes.CDLL(LIB_PATH)
+    path = LIB_PATH
+    if os.environ.get("LJ_LIBRARY") == "check":   # the memory-safety build (bounds checks that trap)
+        path = os.path.join(os.path.dirname(LIB_PATH), "liblj_check.so")
+    if not os.path.exists(path):
+        raise ImportError(f"{os.path.basename(path)} not built ({path}); run python -c "
+                          "'import __graft_entry__ as g; g.build()'")
+    L = ctypes.CDLL(path)
     vp, i64, i32, d, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
     st = ctypes.c_int
     sig = {

@@ -169,3 +169,30 @@ def test_product_binding_has_no_cpu_fallback():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_bounds_checked_build_has_the_checks():
+    """liblj_check.so (-DLJ_CHECK, the memory-safety build run by tests/test_gpu_checked.py)
+    carries device-side traps in the force, energy and list kernels; liblj.so has none."""
+    import shutil
+    import subprocess
+    from paper_1806_05713_b200 import build
+    if shutil.which("cuobjdump") is None and not os.path.exists("/usr/local/cuda/bin/cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    lib, chk = build.build(), build.build(check=True)
+
+    def traps(path):
+        out = subprocess.run([tool, "-sass", path], capture_output=True, text=True).stdout
+        fn, hits = None, {}
+        for line in out.splitlines():
+            if "Function :" in line:
+                fn = line.split("Function :")[1].strip()
+            elif "BPT.TRAP" in line and fn:
+                hits[fn] = hits.get(fn, 0) + 1
+        return hits
+
+    assert not traps(lib)
+    hits = traps(chk)
+    for kernel in ("k_force", "k_energy", "k_list_v4", "k_list_fallback", "k_force_ordered"):
+        assert any(kernel in f for f in hits), kernel
