@@ -576,10 +576,15 @@ def main():
                 return ci.record_event()
 
         def d2h(dst, src, c):
-            co.wait_event(stream.record_event())
+            return d2h_after(dst, src, c, stream.record_event())
+
+        def d2h_after(dst, src, c, ready):
+            co.wait_event(ready)
             with torch.cuda.stream(co):
                 dst[cs[c]].copy_(src[cs[c]], non_blocking=True)
                 return co.record_event()
+
+        p_ready = [None] * K
 
         resorts = 0
         for _ in range(args.steps):
@@ -598,16 +603,22 @@ def main():
                 else:
                     be.force_rows(sim.q, sim.p, w.dt, sim.lst, cb[c], cb[c + 1], sim.counter)
                 lj.unpack_aos4(pd[cb[c]:cb[c + 1]], out=p_out[cs[c]])
-                ev_pout[c] = d2h(ph, p_out, c)   # p is final after the kick (unless re-sorted)
+                p_ready[c] = stream.record_event()   # p is final after the kick (unless re-sorted)
             if not force_only:
                 sim.drift_and_exchange()
+            p_src = p_out
             if sim.p is not pd:                   # a rebuild re-sorted the atoms: p again
                 resorts += 1
                 lj.unpack_aos4(sim.p[rb:re_], out=p_out2)
-                ev_pout = [d2h(ph, p_out2, c) for c in range(K)]
+                p_ready = [stream.record_event()] * K
+                p_src = p_out2
+            # q leaves first: the next step's force needs all of it back, while p's way back
+            # (and the next H2D of a p chunk) only gates that chunk's force
             for c in range(K):
                 lj.unpack_aos4(sim.q[cb[c]:cb[c + 1]], out=q_out[cs[c]])
                 ev_qout[c] = d2h(qh, q_out, c)
+            for c in range(K):
+                ev_pout[c] = d2h_after(ph, p_src, c, p_ready[c])
         for c in range(K):
             stream.wait_event(ev_qout[c])
             stream.wait_event(ev_pout[c])
