@@ -396,8 +396,9 @@ def main():
                 md_graph = sim.graph_collective(args.steps)
             else:
                 md_graph = sim.graph(args.steps, energy_every=every)
-        except (lj.LJError, ValueError) as ex:   # eager GPU steps instead
-            graph_note = f" (graph unavailable: {ex})"
+        except Exception as ex:   # noqa: BLE001 -- any capture failure: eager GPU steps instead, said in the line
+            torch.cuda.synchronize()
+            graph_note = f" (graph unavailable: {type(ex).__name__}: {ex})"
     lj_graph_launches = [0]
     sim.interactions()   # reset counter
     reb0 = sim.stats.rebuilds
