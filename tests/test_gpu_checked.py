@@ -18,8 +18,13 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-SUBSET = ("list or force_parity or ordered or half_cells or overflow or deferred or padding or "
-          "cutoff_edge or counterexample or graph or nve or rebuild or energy")
+# every builder path, every force kernel family (default lanes, index vectors, the ordered,
+# half-cells and variant kernels), energy, and the step graphs -- a few minutes, not the full matrix
+SUBSET = ("list or ordered or overflow or deferred or padding or counterexample or step_graph or rebuild or "
+          "half_cells or variants_at or energy")
+NODES = ([f"tests/test_gpu_parity.py::test_force_parity[{lanes}-{half}-{cfg}]"
+          for lanes in (0, 772, 66052) for half in (True, False) for cfg in (1, 3)]
+         + [f"tests/test_gpu_cutoff.py::test_force_at_cutoff_edge[{half}-772]" for half in (False, True)])
 
 
 def test_parity_suite_under_bounds_checks():
@@ -29,9 +34,9 @@ def test_parity_suite_under_bounds_checks():
     build.build()
     build.build(check=True)
     env = dict(os.environ, LJ_LIBRARY="check")
-    cmd = [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", "-k", SUBSET,
-           os.path.join(ROOT, "tests", "test_gpu_parity.py"), os.path.join(ROOT, "tests", "test_gpu_cutoff.py"),
-           os.path.join(ROOT, "tests", "test_gpu_md.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=2400, env=env, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
-    assert " passed" in r.stdout
+    for args in (["-k", SUBSET, "tests/test_gpu_parity.py", "tests/test_gpu_cutoff.py", "tests/test_gpu_md.py"],
+                 NODES):
+        cmd = [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", *args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=2400, env=env, cwd=ROOT)
+        assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+        assert " passed" in r.stdout
