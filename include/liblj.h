@@ -366,8 +366,11 @@ lj_status lj_md_graph_destroy(lj_md_graph *gr);
 /* ---- the multi-rank step under the caller's stream capture (P > 1; SURVEY
  * §8(f) NEXT-1 "capture the whole step, NCCL included, in a CUDA graph") ---- */
 
-/* Buffers of one rank's bookkeeping rebuild (fixed row ownership, no re-sort:
- * SURVEY §8(e)); device memory owned by the caller. */
+/* Buffers of one rank's bookkeeping rebuild (rows split into
+ * equal slabs); device memory owned by the caller.  Without
+ * reorder the atoms keep their storage slots; with reorder every rebuild
+ * re-sorts them into cell order as lj_rebuild does (the fast path of the list
+ * builder needs cell-ordered storage). */
 typedef struct {
     double *q;                /* n records: replicated positions (complete after the position exchange) */
     double *q_ref;            /* n records: bookkeeping reference (written by every rebuild) */
