@@ -498,6 +498,7 @@ def main():
                              + ", ".join(lanes_str(x) for x in probes),
                 "kernel": f"k_force (full list, lanes_per_row {lanes_str(lj.default_lanes(rows_own, False))})",
                 "force_ms": force_avg, "force_ms_source": force_note,
+                "force_ms_median": statistics.median(force_ms), "force_ms_min": min(force_ms),
                 "best_replay": {"lanes_per_row": lanes_str(best_lanes), "ms": best_ms},
                 "replay_ms": {lanes_str(k): v for k, v in probes.items()},
                 "bytes_per_entry": BYTES_PER_ENTRY, "bytes_per_row": BYTES_PER_ROW, "entries_per_launch": E,

@@ -157,9 +157,6 @@ lj_status lj_force_step(const double *q, double *p, int64_t n, lj_geom g, double
 /* lanes_per_row flag: the list indices are read V = U (2 or 4) at a time with
  * one 64/128-bit load per thread (fewer L1 requests for the index stream). */
 #define LJ_LANES_IDXV (1 << 16)
-/* lanes_per_row flag (G in 4, 8; U in 2, 3): the list indices are loaded without L1
- * allocation and with an L2 evict-first policy (measured variant). */
-#define LJ_LANES_IDX_STREAM (1 << 17)
 
 /* Tuning / instrumentation variant of lj_force_step.
  * lanes_per_row = G | (U << 8) [| LJ_LANES_IDXV]: G (1,2,4,8,16,32) threads

@@ -301,22 +301,18 @@ lj_status lj_force_step_ex(const double* q, double* p, int64_t n, lj_geom g, dou
     if (rows > 0 && (!q || !p || !number_of_partners || !pointer))
         return fail(LJ_ERR_ARG, "force: null pointer");
     if (!aligned32(q) || !aligned32(p)) return fail(LJ_ERR_ARG, "force: q/p not 32-byte aligned");
-    if (lanes_per_row & ~(0xffff | LJ_LANES_IDXV | LJ_LANES_IDX_STREAM))
+    if (lanes_per_row & ~(0xffff | LJ_LANES_IDXV))
         return fail(LJ_ERR_ARG, "force: unknown lanes_per_row bits 0x%x", lanes_per_row);
-    if ((lanes_per_row & 0xff) == 0) lanes_per_row = lj_default_lanes(row_end - row_begin, half) |
-                                                     (lanes_per_row & LJ_LANES_IDX_STREAM);
+    if ((lanes_per_row & 0xff) == 0) lanes_per_row = lj_default_lanes(row_end - row_begin, half);
     int lanes = lanes_per_row & 0xff, unroll = (lanes_per_row >> 8) & 0xff;
     const int idxv = lanes_per_row & LJ_LANES_IDXV;
-    const int stream_idx = lanes_per_row & LJ_LANES_IDX_STREAM;
-    if (stream_idx && (idxv || (lanes != 4 && lanes != 8) || (unroll != 0 && unroll != 2 && unroll != 3)))
-        return fail(LJ_ERR_ARG, "force: LJ_LANES_IDX_STREAM needs G in 4, 8 and U in 2, 3");
     if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && (lanes != 32 || idxv))
         return fail(LJ_ERR_ARG, "force: lanes_per_row G must be 1,2,4,8,16 or 32 (not 32 with LJ_LANES_IDXV) (got %d)",
                     lanes_per_row);
     if (idxv ? (unroll != 2 && unroll != 4) : (unroll != 0 && unroll != 2 && unroll != 3 && unroll != 4))
         return fail(LJ_ERR_ARG, "force: unroll (lanes_per_row >> 8) must be 0, 2, 3 or 4 (2 or 4 with "
                     "LJ_LANES_IDXV) (got %d)", unroll);
-    lanes |= unroll << 8 | idxv | stream_idx;
+    lanes |= unroll << 8 | idxv;
     ForceArgs a;
     a.q = q;
     a.n = n;

@@ -122,28 +122,11 @@ __device__ __forceinline__ void count_interactions(unsigned cnt, unsigned long l
 // are corrected per component and r^2 recomputed.
 // U = 2: at most 48 registers -> 5 CTAs (40 warps) per SM; measured 0.79 vs 0.83 ms
 // (54 registers, 4 CTAs) on config 4 -- the kernel is latency/L1-bound, warps help.
-// The list index stream (4 B per entry, read once) through L1 without allocating and
-// with an L2 evict-first policy, so that it does not displace the partner records
-// (LJ_LANES_IDX_STREAM, measured variant).
-template <bool STREAM>
-__device__ __forceinline__ int load_index(const int32_t* a, uint64_t policy) {
-    if (!STREAM) return __ldg(a);
-    int v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(policy));
-    return v;
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-template <int G, int U, bool HALF, bool STREAM = false>
+template <int G, int U, bool HALF>
 __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
     k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
             const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
             PairConsts c, unsigned long long* n_inter) {
-    const uint64_t pol = STREAM ? evict_first_policy() : 0;
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t r = t / G;
     const int g = threadIdx.x % G;
@@ -158,7 +141,7 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
     // indices of chunk k+1 are loaded before the records of chunk k are used
     int jn[U];
 #pragma unroll
-    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? load_index<STREAM>(lst + g + u * G, pol) : -1;
+    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
     for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
         int j[U];
         rec4 qj[U];
@@ -171,7 +154,7 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int kn = k0 + U * G + u * G;
-            jn[u] = kn < n ? load_index<STREAM>(lst + kn, pol) : -1;
+            jn[u] = kn < n ? __ldg(lst + kn) : -1;
         }
         double dx[U], dy[U], dz[U], r2[U];
         int hmax = 0;
@@ -882,7 +865,7 @@ PairConsts make_consts(const ForceArgs& a) {
     return c;
 }
 
-template <bool HALF, int U, bool STREAM = false>
+template <bool HALF, int U>
 cudaError_t launch_g(const ForceArgs& a, int lanes, cudaStream_t s) {
     if (a.rows <= 0) return cudaSuccess;
     PairConsts c = make_consts(a);
@@ -891,8 +874,8 @@ cudaError_t launch_g(const ForceArgs& a, int lanes, cudaStream_t s) {
     const rec4* q = (const rec4*)a.q;
     rec4* p = (rec4*)a.p;
 #define LJ_LAUNCH(G)                                                                                        \
-    k_force<G, U, HALF, STREAM><<<grid, kForceThreads, 0, s>>>(q, p, a.row_begin, a.rows, a.npart, a.ptr, a.list, \
-                                                             c, a.n_inter)
+    k_force<G, U, HALF><<<grid, kForceThreads, 0, s>>>(q, p, a.row_begin, a.rows, a.npart, a.ptr, a.list, c, \
+                                                     a.n_inter)
     switch (lanes) {
         case 1: LJ_LAUNCH(1); break;
         case 2: LJ_LAUNCH(2); break;
@@ -942,12 +925,6 @@ cudaError_t launch_gu(const ForceArgs& a, int lanes, cudaStream_t s) {
     if (lanes & LJ_LANES_IDXV) {
         if (U == 4) return launch_idxv<HALF, 4>(a, G, s);
         if (U == 2) return launch_idxv<HALF, 2>(a, G, s);
-        return cudaErrorInvalidValue;
-    }
-    if (lanes & LJ_LANES_IDX_STREAM) {
-        if (G != 4 && G != 8) return cudaErrorInvalidValue;
-        if (U == 3) return launch_g<HALF, 3, true>(a, G, s);
-        if (U == 0 || U == 2) return launch_g<HALF, 2, true>(a, G, s);
         return cudaErrorInvalidValue;
     }
     if (U == 4) return launch_g<HALF, 4>(a, G, s);

@@ -20,7 +20,6 @@ LIB_PATH = os.path.join(_HERE, "liblj.so")
 LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 LJ_LIST_PADDED, LJ_LIST_DEFERRED, LJ_PADDED_ROW_STRIDE = 1, 2, 196   # include/liblj.h
 LJ_LANES_IDXV = 1 << 16   # include/liblj.h: index vector loads (lanes_per_row = G | V << 8 | LJ_LANES_IDXV)
-LJ_LANES_IDX_STREAM = 1 << 17   # include/liblj.h: index loads with L1 no-allocate + L2 evict-first
 LAYOUTS = {"aos4": 0, "soa": 1, "aos3": 2, "aos8": 3}                    # LJ_LAYOUT_*
 RECIPROCALS = {"newton3": 0, "newton2": 1, "approx": 2, "ieee": 3}       # LJ_RCP_*
 
