@@ -1,4 +1,5 @@
-"""List-build timing on one GPU (development tool): compact and padded layouts,
+"""List-build timing on one GPU (development tool): compact and padded layouts
+(lj_build_list_ex) and the padded lj_rebuild,
 configs 3 (cell order) and 4 (cell order).  One JSON object per measurement."""
 import json
 import os
@@ -39,6 +40,15 @@ def main():
                 ms = timeit(lambda: b.build(q))
                 print(json.dumps(dict(cfg=c, half=half, padded=padded, what="build", ms=round(ms, 4),
                                       entries=lst.n_entries)), flush=True)
+                if padded and not half:
+                    # lj_rebuild (wrap + cell-order permutation + list): the MD path's builder
+                    q_out, p_in = torch.empty_like(q), torch.zeros_like(q)
+                    p_out, perm = torch.empty_like(q), torch.empty(w.n, dtype=torch.int64, device=dev)
+                    lst = b.rebuild(q, p_in, q_out, p_out, None, perm)
+                    ms = timeit(lambda: b.rebuild(q, p_in, q_out, p_out, None, perm))
+                    print(json.dumps(dict(cfg=c, half=half, padded=padded, what="rebuild", ms=round(ms, 4),
+                                          entries=lst.n_entries)), flush=True)
+                    del q_out, p_in, p_out, perm
                 del b, lst
                 torch.cuda.empty_cache()
 
