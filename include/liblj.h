@@ -100,6 +100,18 @@ lj_status lj_build_list(const double *q, int64_t n, lj_geom g, int half,
  * caller reads them after a later synchronisation (the MD driver: at the next
  * displacement readback), so a rebuild costs no host round trip. */
 #define LJ_LIST_DEFERRED 2
+/* With LJ_LIST_PADDED only: the rows in blocks of 8 (rows row_begin + 8b ..
+ * + 8b + 7), their entries interleaved in granules of 4 -- granule k of a block
+ * holds entries 4k..4k+3 of its row 0, then of its row 1, ..., of its row 7
+ * -- so that the force kernel's index loads (4 lanes per row, 8
+ * rows per warp) are one 128-byte line each.  pointer[r] = the position of
+ * row r's entry 0 with bit 62 set (LJ_LIST_IL_BIT); entry e of row r is at
+ * (pointer[r] & (LJ_LIST_IL_BIT - 1)) + e + 28 * (e / 4); pointer[rows] = the
+ * padded extent.  capacity must be >= ceil(rows / 8) * 8 * LJ_PADDED_ROW_STRIDE.
+ * Every consumer of a list in this library (force, energy, row
+ * classification) reads compact, padded and interleaved lists alike. */
+#define LJ_LIST_INTERLEAVED 4
+#define LJ_LIST_IL_BIT (1LL << 62)
 #ifndef LJ_PADDED_ROW_STRIDE
 /* 196 entries = 784 B: not a multiple of the 128-B line, so the rows a warp
  * reads do not all start on the same DRAM channel / L2 slice (strides of 640 or
@@ -108,7 +120,8 @@ lj_status lj_build_list(const double *q, int64_t n, lj_geom g, int half,
 #endif
 
 /* lj_build_list with layout flags (0 = compact CSR, as lj_build_list).  With
- * LJ_LIST_PADDED, capacity must be >= rows * LJ_PADDED_ROW_STRIDE (else
+ * LJ_LIST_PADDED, capacity must be >= rows * LJ_PADDED_ROW_STRIDE (rows rounded
+ * up to a multiple of 8 with LJ_LIST_INTERLEAVED; else
  * LJ_ERR_CAPACITY, *n_entries = that size); *n_entries receives the number of
  * valid entries; a row longer than the stride returns LJ_ERR_UNSUPPORTED (use
  * the compact layout).  Same synchronisation as lj_build_list. */
@@ -339,6 +352,7 @@ typedef struct {
     int energy_every;         /* 0, or sample (KE, PE) at steps k % energy_every == 0 of every launch: the
                                  kick is split in two halves around lj_energy (reading O8, synchronised p) */
     double *energies;         /* 2 doubles per sample (ceil(steps / energy_every) samples), if energy_every */
+    int interleaved;          /* the list is LJ_LIST_INTERLEAVED (rebuilds keep that layout; capacity as there) */
 } lj_md_graph_desc;
 
 typedef struct lj_md_graph lj_md_graph;
@@ -397,6 +411,7 @@ typedef struct {
                                  (n records, rows [k n_own, (k+1) n_own) valid; peer-mapped, e.g. CUDA
                                  IPC), current when the rebuild runs -- see lj_copy_records */
     int64_t n_own;            /* rows per rank (equal slabs; own rows = one slab) */
+    int interleaved;          /* the list is LJ_LIST_INTERLEAVED (rebuilds keep that layout; capacity as there) */
 } lj_md_rebuild_desc;
 
 /* Called while `stream` is being captured into a CUDA graph (cudaStreamBeginCapture

@@ -145,9 +145,10 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
     LJ_TRY(check_n(n));
     LJ_TRY(check_geom(g, true));
     LJ_TRY(check_rows(n, row_begin, row_end));
-    if (flags & ~(LJ_LIST_PADDED | LJ_LIST_DEFERRED)) return fail(LJ_ERR_ARG, "build_list: unknown flags 0x%x", flags);
-    if ((flags & LJ_LIST_DEFERRED) && !(flags & LJ_LIST_PADDED))
-        return fail(LJ_ERR_ARG, "build_list: LJ_LIST_DEFERRED needs LJ_LIST_PADDED");
+    if (flags & ~(LJ_LIST_PADDED | LJ_LIST_DEFERRED | LJ_LIST_INTERLEAVED))
+        return fail(LJ_ERR_ARG, "build_list: unknown flags 0x%x", flags);
+    if ((flags & (LJ_LIST_DEFERRED | LJ_LIST_INTERLEAVED)) && !(flags & LJ_LIST_PADDED))
+        return fail(LJ_ERR_ARG, "build_list: LJ_LIST_DEFERRED / LJ_LIST_INTERLEAVED need LJ_LIST_PADDED");
     if (half && (row_begin != 0 || row_end != n))
         return fail(LJ_ERR_UNSUPPORTED, "half list must cover all rows [0,n) (SURVEY §8(e))");
     if (!n_entries || !pointer || (row_end > row_begin && !number_of_partners) || (n > 0 && !q))
@@ -163,8 +164,10 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
     char* ws = (char*)workspace;
     const int64_t rows = row_end - row_begin;
     const bool padded = (flags & LJ_LIST_PADDED) != 0;
-    if (padded && capacity < rows * (int64_t)LJ_PADDED_ROW_STRIDE) {
-        *n_entries = rows * (int64_t)LJ_PADDED_ROW_STRIDE;
+    const bool il = (flags & LJ_LIST_INTERLEAVED) != 0;
+    const int64_t padded_size = (il ? (rows + 7) / 8 * 8 : rows) * (int64_t)LJ_PADDED_ROW_STRIDE;
+    if (padded && capacity < padded_size) {
+        *n_entries = padded_size;
         return fail(LJ_ERR_CAPACITY, "build_list: padded layout needs capacity %lld", (long long)*n_entries);
     }
     int64_t* counts_scan = padded ? (int64_t*)(ws + W.off_ptrtmp) : pointer;
@@ -175,7 +178,7 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
         LJ_CUDA(launch_cells(q, n, cg, ws, W, s), "lj_build_list/cells");
     if (rows > 0)
         LJ_CUDA(launch_list_pass1(q, cg, g.rs, half, row_begin, row_end, number_of_partners,
-                                  padded ? sorted_list : nullptr, ws, W, s),
+                                  padded ? sorted_list : nullptr, ws, W, s, il),
                 "lj_build_list/pass1");
     LJ_CUDA(launch_scan_i32_to_i64(number_of_partners, counts_scan, rows, (int64_t*)(ws + W.off_scan),
                                    W.scan_blocks, s),
@@ -184,7 +187,7 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
         LJ_CUDA(launch_build_status(counts_scan + rows, rows > 0 ? list_row_overflow_flag(ws, W) : nullptr,
                                     dev_status, s),
                 "lj_md_graph/status");
-        LJ_CUDA(launch_padded_pointer(pointer, rows, s), "lj_md_graph/pointer");
+        LJ_CUDA(launch_padded_pointer(pointer, rows, s, il), "lj_md_graph/pointer");
         return LJ_OK;
     }
     if (flags & LJ_LIST_DEFERRED) {   // status to the caller's pinned memory, no synchronisation
@@ -194,7 +197,7 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
             LJ_CUDA(cudaMemcpyAsync(n_entries + 1, list_row_overflow_flag(ws, W), sizeof(int32_t),
                                     cudaMemcpyDeviceToHost, s),
                     "lj_build_list/status");
-        LJ_CUDA(launch_padded_pointer(pointer, rows, s), "lj_build_list/pointer");
+        LJ_CUDA(launch_padded_pointer(pointer, rows, s, il), "lj_build_list/pointer");
         return LJ_OK;
     }
     int64_t total = 0;
@@ -211,7 +214,7 @@ lj_status build_list_impl(const double* q, int64_t n, lj_geom g, int half, int64
         if (row_overflow)
             return fail(LJ_ERR_UNSUPPORTED, "build_list: a row has more than %d partners; use the compact layout",
                         LJ_PADDED_ROW_STRIDE);
-        LJ_CUDA(launch_padded_pointer(pointer, rows, s), "lj_build_list/pointer");
+        LJ_CUDA(launch_padded_pointer(pointer, rows, s, il), "lj_build_list/pointer");
         return LJ_OK;
     }
     if (total > capacity)
@@ -598,9 +601,8 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
         return fail(LJ_ERR_ARG, "md_graph: null pointer");
     if (!aligned32(d->q) || !aligned32(d->p) || !aligned32(d->q_ref) || !aligned32(d->q_alt) || !aligned32(d->p_alt))
         return fail(LJ_ERR_ARG, "md_graph: records not 32-byte aligned");
-    if (d->capacity < n * (int64_t)LJ_PADDED_ROW_STRIDE)
-        return fail(LJ_ERR_CAPACITY, "md_graph: the padded list needs capacity %lld",
-                    (long long)(n * (int64_t)LJ_PADDED_ROW_STRIDE));
+    const int64_t need = (d->interleaved ? (n + 7) / 8 * 8 : n) * (int64_t)LJ_PADDED_ROW_STRIDE;
+    if (d->capacity < need) return fail(LJ_ERR_CAPACITY, "md_graph: the padded list needs capacity %lld", (long long)need);
     const CellGrid cg = make_grid(d->g);
     const BuildWorkspace W = build_workspace_layout(n, cg.ncell, n);
     if (d->workspace_bytes < W.total) return fail(LJ_ERR_ARG, "md_graph: workspace too small");
@@ -692,9 +694,10 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
              "md_graph/capture-body");
         l0 = g_launches;
         lj_status st = LJ_OK;
+        const int lflags = LJ_LIST_PADDED | (d->interleaved ? LJ_LIST_INTERLEAVED : 0);
         if (d->reorder) {   // as lj_rebuild, then the permuted state back into q / p
             RebuildIO io{d->q, d->p, d->q_alt, d->p_alt, d->q_ref, d->perm, PeerMomenta()};
-            st = build_list_impl(d->q_alt, n, d->g, 0, 0, n, LJ_LIST_PADDED, d->number_of_partners, d->pointer,
+            st = build_list_impl(d->q_alt, n, d->g, 0, 0, n, lflags, d->number_of_partners, d->pointer,
                                  d->sorted_list, d->capacity, d->status + 2, d->workspace, d->workspace_bytes, cs,
                                  &io, d->status);
             if (st == LJ_OK) e = cudaMemcpyAsync(d->q, d->q_alt, rec, cudaMemcpyDeviceToDevice, cs);
@@ -703,7 +706,7 @@ lj_status lj_md_graph_create(const lj_md_graph_desc* d, lj_md_graph** out) {
         } else {            // wrap + snapshot, then the list (as lj_wrap + lj_build_list_ex)
             e = launch_wrap(d->q, d->q_ref, n, d->g.L, cs);
             if (e == cudaSuccess)
-                st = build_list_impl(d->q, n, d->g, 0, 0, n, LJ_LIST_PADDED, d->number_of_partners, d->pointer,
+                st = build_list_impl(d->q, n, d->g, 0, 0, n, lflags, d->number_of_partners, d->pointer,
                                      d->sorted_list, d->capacity, d->status + 2, d->workspace, d->workspace_bytes,
                                      cs, nullptr, d->status);
         }
@@ -744,9 +747,9 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long 
         if (d->q_alt == d->q || d->p_alt == d->p) return fail(LJ_ERR_ARG, "md_capture_rebuild: alt buffers must differ");
     }
     const int64_t rows = d->row_end - d->row_begin;
-    if (d->capacity < rows * (int64_t)LJ_PADDED_ROW_STRIDE)
-        return fail(LJ_ERR_CAPACITY, "md_capture_rebuild: the padded list needs capacity %lld",
-                    (long long)(rows * (int64_t)LJ_PADDED_ROW_STRIDE));
+    const int64_t need = (d->interleaved ? (rows + 7) / 8 * 8 : rows) * (int64_t)LJ_PADDED_ROW_STRIDE;
+    if (d->capacity < need)
+        return fail(LJ_ERR_CAPACITY, "md_capture_rebuild: the padded list needs capacity %lld", (long long)need);
     const CellGrid cg = make_grid(d->g);
     const BuildWorkspace W = build_workspace_layout(n, cg.ncell, n);
     if (d->workspace_bytes < W.total) return fail(LJ_ERR_ARG, "md_capture_rebuild: workspace too small");
@@ -778,6 +781,7 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long 
                                                   cudaStreamCaptureModeRelaxed);
     const long long l0 = g_launches;
     lj_status st = LJ_OK;
+    const int lflags = LJ_LIST_PADDED | (d->interleaved ? LJ_LIST_INTERLEAVED : 0);
     if (e == cudaSuccess) {
         if (d->reorder) {
             // as lj_rebuild -- wrap, cells, the cell-order permutation of q (replicated) and q_ref --
@@ -788,7 +792,7 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long 
             io.pm.n_own = d->n_own;
             io.pm.own_lo = d->row_begin;
             io.pm.own_hi = d->row_end;
-            st = build_list_impl(d->q_alt, n, d->g, 0, d->row_begin, d->row_end, LJ_LIST_PADDED,
+            st = build_list_impl(d->q_alt, n, d->g, 0, d->row_begin, d->row_end, lflags,
                                  d->number_of_partners, d->pointer, d->sorted_list, d->capacity, d->status + 2,
                                  d->workspace, d->workspace_bytes, bs, &io, d->status);
             const size_t rec = sizeof(double) * 4;
@@ -799,7 +803,7 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc* d, void* stream, long 
         } else {
             e = launch_wrap(d->q, d->q_ref, n, d->g.L, bs);
             if (e == cudaSuccess)
-                st = build_list_impl(d->q, n, d->g, 0, d->row_begin, d->row_end, LJ_LIST_PADDED,
+                st = build_list_impl(d->q, n, d->g, 0, d->row_begin, d->row_end, lflags,
                                      d->number_of_partners, d->pointer, d->sorted_list, d->capacity, d->status + 2,
                                      d->workspace, d->workspace_bytes, bs, nullptr, d->status);
         }

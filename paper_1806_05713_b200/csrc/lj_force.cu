@@ -122,27 +122,32 @@ __device__ __forceinline__ void count_interactions(unsigned cnt, unsigned long l
 // are corrected per component and r^2 recomputed.
 // U = 2: at most 48 registers -> 5 CTAs (40 warps) per SM; measured 0.79 vs 0.83 ms
 // (54 registers, 4 CTAs) on config 4 -- the kernel is latency/L1-bound, warps help.
-template <int G, int U, bool HALF>
-__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
-    k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
-            const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
-            PairConsts c, unsigned long long* n_inter) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t r = t / G;
-    const int g = threadIdx.x % G;
-    const bool active = r < rows;
-    double ax = 0.0, ay = 0.0, az = 0.0;
-    unsigned cnt = 0;
-    const int64_t i = row_begin + (active ? r : 0);
-    const rec4 qi = load_rec(q, active ? i : 0);
-    const int32_t* __restrict__ lst = list + (active ? ptr[r] : 0);
-    const int n = active ? npart[r] : 0;
+// Offset of a row's entry e from the row base: e (compact and padded lists) or, in
+// the interleaved layout (LJ_LIST_INTERLEAVED), e + 28 (e / 4).  For G % 4 == 0 the
+// entries a lane reads are e and e + d with d a multiple of 4, whose interleaved
+// offsets differ by 8 d: the chunk loop then keeps compile-time load offsets in
+// both layouts (LIN below) and the interleaved list costs no extra instructions.
+template <bool IL>
+__device__ __forceinline__ int eoff(int e) {
+    return IL ? e + kIlSkip * (e >> 2) : e;
+}
+
+// One row's chunk loop of k_force (a G-lane group; accumulates into ax..cnt).
+template <int G, int U, bool HALF, bool IL>
+__device__ __forceinline__ void force_row_loop(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t i,
+                                               const rec4& qi, const int32_t* __restrict__ lst, int n, int g,
+                                               const PairConsts& c, double& ax, double& ay, double& az,
+                                               unsigned& cnt) {
+    constexpr bool LIN = !IL || (G % kIlGran == 0);   // offsets linear in the entry index
+    constexpr int F = IL ? kIlRows : 1;               // (LIN) offset step per entry
     // software pipeline (the GPU analogue of the paper's SWP): the
     // indices of chunk k+1 are loaded before the records of chunk k are used
     int jn[U];
+    int ko = eoff<IL>(g);   // offset of entry k0 (LIN)
 #pragma unroll
-    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
-    for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
+    for (int u = 0; u < U; u++)
+        jn[u] = (g + u * G < n) ? __ldg(lst + (LIN ? ko + F * u * G : eoff<IL>(g + u * G))) : -1;
+    for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G, ko += F * U * G) {
         int j[U];
         rec4 qj[U];
 #pragma unroll
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int kn = k0 + U * G + u * G;
-            jn[u] = kn < n ? __ldg(lst + kn) : -1;
+            jn[u] = kn < n ? __ldg(lst + (LIN ? ko + F * (U * G + u * G) : eoff<IL>(kn))) : -1;
         }
         double dx[U], dy[U], dz[U], r2[U];
         int hmax = 0;
@@ -200,6 +205,41 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
             accumulate();
         }
     }
+}
+
+// G lanes per row, U independent partner gathers in flight per lane.
+// Full list: no atomics, p_i committed once by lane 0 of the group.
+// Half list: p_j += df r by fp64 REDs, p_i committed by REDs as well.
+// The chunk loop runs while ANY row of the warp has entries left (warp-uniform
+// trip count), so the minimum-image test can be one vote per chunk: r^2 of the
+// raw differences below (L/2)^2 (integer test on the high words) proves that no
+// component needs an image; otherwise (rows near a box face) the differences
+// are corrected per component and r^2 recomputed.  The list layout (plain or
+// interleaved; every row of a list has the same) is taken per warp by a vote.
+// U = 2: at most 48 registers -> 5 CTAs (40 warps) per SM; measured 0.79 vs 0.83 ms
+// (54 registers, 4 CTAs) on config 4 -- the kernel is latency/L1-bound, warps help.
+template <int G, int U, bool HALF>
+__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
+    k_force(const rec4* __restrict__ q, rec4* __restrict__ p, int64_t row_begin, int64_t rows,
+            const int32_t* __restrict__ npart, const int64_t* __restrict__ ptr, const int32_t* __restrict__ list,
+            PairConsts c, unsigned long long* n_inter) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    const bool active = r < rows;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    unsigned cnt = 0;
+    const int64_t i = row_begin + (active ? r : 0);
+    const rec4 qi = load_rec(q, active ? i : 0);
+    const int64_t p0 = active ? ptr[r] : 0;
+    const int32_t* __restrict__ lst = list + (p0 & (kIlBit - 1));
+    const int n = active ? npart[r] : 0;
+    const bool il = __any_sync(0xffffffffu, (p0 & kIlBit) != 0);
+    LJ_CHECK_THAT(!active || il == ((p0 & kIlBit) != 0));
+    if (il)
+        force_row_loop<G, U, HALF, true>(q, p, i, qi, lst, n, g, c, ax, ay, az, cnt);
+    else
+        force_row_loop<G, U, HALF, false>(q, p, i, qi, lst, n, g, c, ax, ay, az, cnt);
     unsigned cnt_row = cnt;
     group_reduce<G>(ax, ay, az, cnt_row);
     if (active && g == 0) {
@@ -264,9 +304,9 @@ __global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
     const int64_t i = row_begin + (active ? r : 0);
     const rec4 qi = load_rec(q, i);
     int64_t base = 0;
-    int off = 0, end = 0;
+    int off = 0, end = 0, skip = 0;
     if (active) {
-        const int64_t p0 = ptr[r];
+        const int64_t p0 = row_decode(list, ptr[r], skip) - list;   // (interleaved rows: 4-aligned, off = 0)
         base = p0 & ~(int64_t)(V - 1);
         off = (int)(p0 - base);
         end = off + npart[r];
@@ -275,7 +315,7 @@ __global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
     // software pipeline: the next chunk's index vector is loaded before this chunk's records are used
     int jn[V];
     if (V * g < end) {
-        IdxVec<V>::load(win + V * g, jn);
+        IdxVec<V>::load(win + il_off(V * g, skip), jn);
     } else {
 #pragma unroll
         for (int u = 0; u < V; u++) jn[u] = -1;
@@ -291,7 +331,7 @@ __global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
         }
         const int sn = s0 + V * G;
         if (sn < end) {
-            IdxVec<V>::load(win + sn, jn);
+            IdxVec<V>::load(win + il_off(sn, skip), jn);
         } else {
 #pragma unroll
             for (int u = 0; u < V; u++) jn[u] = -1;
@@ -489,12 +529,13 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
             const bool active = base + grp < ccnt;
             const int64_t i = cs + (active ? base + grp : 0);
             const rec4 qi = load_rec(q, i);
-            const int32_t* __restrict__ lst = list + (active ? ptr[i] : 0);
+            int skip;
+            const int32_t* __restrict__ lst = row_decode(list, active ? ptr[i] : 0, skip);
             const int n = active ? npart[i] : 0;
             double ax = 0.0, ay = 0.0, az = 0.0;
             int jn[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
+            for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + il_off(g + u * G, skip)) : -1;
             for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
                 int j[U];
                 rec4 qj[U];
@@ -507,7 +548,7 @@ __global__ void __launch_bounds__(kHalfCellThreads, 1024 / kHalfCellThreads)
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int kn = k0 + U * G + u * G;
-                    jn[u] = kn < n ? __ldg(lst + kn) : -1;
+                    jn[u] = kn < n ? __ldg(lst + il_off(kn, skip)) : -1;
                 }
                 double dx[U], dy[U], dz[U], r2[U];
                 int hmax = 0;
@@ -644,11 +685,12 @@ __global__ void __launch_bounds__(kForceThreads, (LAYOUT == LJ_LAYOUT_SOA || LAY
     const int64_t i = row_begin + (active ? r : 0);
     double qix, qiy, qiz;
     Lay::pos(q, n_atoms, active ? i : 0, qix, qiy, qiz);
-    const int32_t* __restrict__ lst = list + (active ? ptr[r] : 0);
+    int skip;
+    const int32_t* __restrict__ lst = row_decode(list, active ? ptr[r] : 0, skip);
     const int n = active ? npart[r] : 0;
     int jn[U];
 #pragma unroll
-    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
+    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + il_off(g + u * G, skip)) : -1;
     for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
         int j[U];
         double dx[U], dy[U], dz[U], r2[U];
@@ -661,7 +703,7 @@ __global__ void __launch_bounds__(kForceThreads, (LAYOUT == LJ_LAYOUT_SOA || LAY
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int kn = k0 + U * G + u * G;
-            jn[u] = kn < n ? __ldg(lst + kn) : -1;
+            jn[u] = kn < n ? __ldg(lst + il_off(kn, skip)) : -1;
         }
         int hmax = 0;
 #pragma unroll
@@ -708,22 +750,18 @@ __global__ void __launch_bounds__(kForceThreads, (LAYOUT == LJ_LAYOUT_SOA || LAY
 // Roofline probe: the force kernel's access pattern (G lanes per row, U gathers
 // in flight per lane, next indices prefetched, the same warp-uniform chunk loop)
 // without the arithmetic.
-template <int G, int U>
-__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
-    k_gather_probe(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
-                   const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* sink) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t r = t / G;
-    const int g = threadIdx.x % G;
-    const bool active = r < rows;
-    const int64_t i = active ? r : 0;
-    const int32_t* __restrict__ lst = list + (active ? ptr[r] : 0);
-    const int n = active ? npart[r] : 0;
+template <int G, int U, bool IL>
+__device__ __forceinline__ double probe_row_loop(const rec4* __restrict__ q, int64_t i,
+                                                 const int32_t* __restrict__ lst, int n, int g) {
+    constexpr bool LIN = !IL || (G % kIlGran == 0);
+    constexpr int F = IL ? kIlRows : 1;
     double s = 0.0;
     int jn[U];
+    int ko = eoff<IL>(g);
 #pragma unroll
-    for (int u = 0; u < U; u++) jn[u] = (g + u * G < n) ? __ldg(lst + g + u * G) : -1;
-    for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G) {
+    for (int u = 0; u < U; u++)
+        jn[u] = (g + u * G < n) ? __ldg(lst + (LIN ? ko + F * u * G : eoff<IL>(g + u * G))) : -1;
+    for (int k0 = g; __any_sync(0xffffffffu, k0 < n); k0 += U * G, ko += F * U * G) {
         rec4 qj[U];
         int j[U];
 #pragma unroll
@@ -734,11 +772,28 @@ __global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int kn = k0 + U * G + u * G;
-            jn[u] = kn < n ? __ldg(lst + kn) : -1;
+            jn[u] = kn < n ? __ldg(lst + (LIN ? ko + F * (U * G + u * G) : eoff<IL>(kn))) : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) s += j[u] >= 0 ? qj[u].x + qj[u].y + qj[u].z : 0.0;
     }
+    return s;
+}
+
+template <int G, int U>
+__global__ void __launch_bounds__(kForceThreads, U == 2 ? 5 : (U == 3 ? 4 : 3))
+    k_gather_probe(const rec4* __restrict__ q, int64_t rows, const int32_t* __restrict__ npart,
+                   const int64_t* __restrict__ ptr, const int32_t* __restrict__ list, double* sink) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = t / G;
+    const int g = threadIdx.x % G;
+    const bool active = r < rows;
+    const int64_t i = active ? r : 0;
+    const int64_t p0 = active ? ptr[r] : 0;
+    const int32_t* __restrict__ lst = list + (p0 & (kIlBit - 1));
+    const int n = active ? npart[r] : 0;
+    const double s = __any_sync(0xffffffffu, (p0 & kIlBit) != 0) ? probe_row_loop<G, U, true>(q, i, lst, n, g)
+                                                                  : probe_row_loop<G, U, false>(q, i, lst, n, g);
     if (s == 1.2345678e300) sink[0] = s;   // never true: keeps the loads alive
 }
 
@@ -753,9 +808,9 @@ __global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
     const bool active = r < rows;
     const int64_t i = active ? r : 0;
     int64_t base = 0;
-    int off = 0, end = 0;
+    int off = 0, end = 0, skip = 0;
     if (active) {
-        const int64_t p0 = ptr[r];
+        const int64_t p0 = row_decode(list, ptr[r], skip) - list;   // (interleaved rows: 4-aligned, off = 0)
         base = p0 & ~(int64_t)(V - 1);
         off = (int)(p0 - base);
         end = off + npart[r];
@@ -764,7 +819,7 @@ __global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
     double s = 0.0;
     int jn[V];
     if (V * g < end) {
-        IdxVec<V>::load(win + V * g, jn);
+        IdxVec<V>::load(win + il_off(V * g, skip), jn);
     } else {
 #pragma unroll
         for (int u = 0; u < V; u++) jn[u] = -1;
@@ -779,7 +834,7 @@ __global__ void __launch_bounds__(kForceThreads, V == 2 ? 5 : 3)
         }
         const int sn = s0 + V * G;
         if (sn < end) {
-            IdxVec<V>::load(win + sn, jn);
+            IdxVec<V>::load(win + il_off(sn, skip), jn);
         } else {
 #pragma unroll
             for (int u = 0; u < V; u++) jn[u] = -1;
@@ -814,11 +869,13 @@ __global__ void __launch_bounds__(kForceThreads)
         const int64_t i = row_begin + r;
         const rec4 qi = load_rec(q, i);
         rec4 pi = p[i];
-        const int64_t beg = ptr[r];
+        int skip;
+        const int32_t* row = row_decode(list, ptr[r], skip);
         const int n = npart[r];
         for (int k = 0; k < n; k++) {
-            LJ_CHECK_THAT(list[beg + k] >= 0 && list[beg + k] < n_atoms);
-            const rec4 qj = load_rec(q, list[beg + k]);
+            const int j = row[il_off(k, skip)];
+            LJ_CHECK_THAT(j >= 0 && j < n_atoms);
+            const rec4 qj = load_rec(q, j);
             double dx = min_image_exact(__dsub_rn(qj.x, qi.x), L);
             double dy = min_image_exact(__dsub_rn(qj.y, qi.y), L);
             double dz = min_image_exact(__dsub_rn(qj.z, qi.z), L);

@@ -48,6 +48,25 @@ __device__ __forceinline__ rec4 load_rec(const rec4* __restrict__ a, int64_t i) 
     return r;
 }
 
+// Interleaved padded list (LJ_LIST_INTERLEAVED): the rows of a
+// padded list in blocks of kIlRows, their entries interleaved in granules of
+// kIlGran -- granule k of the block holds entries [4k, 4k+4) of row 0, then of
+// row 1, ..., row 7 -- so that the index loads of a warp whose 8 rows x 4 lanes
+// read entries 4k..4k+3 of 8 consecutive rows are ONE 128-B line instead of 8
+// (tools/layout_probe.py: the gather replay 14 % faster).  pointer[r] holds the
+// address of the row's entry 0 with bit 62 set; entry e of the row is at
+// pointer + e + kIlSkip * (e / kIlGran).  Every list consumer decodes the row
+// with row_decode, so compact, padded and interleaved lists all read correctly.
+constexpr int kIlRows = 8, kIlGran = 4;
+constexpr int kIlSkip = (kIlRows - 1) * kIlGran;   // 28
+constexpr int64_t kIlBit = 1LL << 62;
+__device__ __forceinline__ const int32_t* row_decode(const int32_t* list, int64_t p0, int& skip) {
+    skip = (p0 & kIlBit) ? kIlSkip : 0;
+    return list + (p0 & (kIlBit - 1));
+}
+// offset of entry e from the row base (skip from row_decode)
+__device__ __forceinline__ int il_off(int e, int skip) { return e + skip * (e >> 2); }
+
 // Cell geometry shared by the list builder and the cell-order pass.
 struct CellGrid {
     double L, inv_w;   // inv_w = nc / L
@@ -83,8 +102,8 @@ cudaError_t launch_rebuild_cells(double* q, const double* p, double* q_out, doub
 // (out == nullptr: the workspace scratch; else the caller's padded list)
 cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
                               int64_t row_end, int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W,
-                              cudaStream_t s);
-cudaError_t launch_padded_pointer(int64_t* ptr, int64_t rows, cudaStream_t s);
+                              cudaStream_t s, bool interleaved = false);
+cudaError_t launch_padded_pointer(int64_t* ptr, int64_t rows, cudaStream_t s, bool interleaved = false);
 // pass 2: scratch -> CSR, or (if some row overflowed the scratch) a direct fill at pointer[r]
 cudaError_t launch_list_pass2(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
                               int64_t row_end, int32_t* npart, const int64_t* ptr, int32_t* list, bool row_overflow,

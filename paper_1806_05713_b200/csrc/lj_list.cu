@@ -302,7 +302,16 @@ struct ListArgs {
     float lo2, hi2;           // fp32 decision band around rs2: r2f < lo2 accept, r2f >= hi2 reject
     float rb2;                // squared reach of a half-cell box (rounded-box candidate screen)
     const struct CellSetup* setups;   // per-cell neighbour runs (k_cell_setup), v4 only
+    int il_skip;              // kIlSkip: out is an interleaved padded list (LJ_LIST_INTERLEAVED), else 0
 };
+
+// Row rr of the non-direct output (the per-row scratch or the caller's padded list):
+// stride kRowCap, or the interleaved layout (entry e of the row at il_off(e, il_skip)).
+__device__ __forceinline__ int32_t* padded_row(int32_t* out, int64_t rr, int il_skip) {
+    return out + (il_skip ? (rr >> 3) * (int64_t)(kIlRows * kRowCap) + (rr & (kIlRows - 1)) * kIlGran
+                          : rr * (int64_t)kRowCap);
+}
+static_assert(kRowCap % kIlGran == 0, "interleaved rows need a stride made of whole granules");
 
 // Exact accept test on raw fp64 coordinates, bit-identical to the oracle's
 // (readings O2/O3): d = x_j - x_i (IEEE), minimum image d -/+ L when |d| > L/2,
@@ -526,9 +535,10 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
                 dst = a.out + a.ptr[r];
                 cap = LLONG_MAX;
             } else {
-                dst = a.out + r * (int64_t)kRowCap;
+                dst = padded_row(a.out, r, a.il_skip);
                 cap = kRowCap;
             }
+            const int skip = DIRECT ? 0 : a.il_skip;
             const int tau = ((fi.x >= midx) << 2) | ((fi.y >= midy) << 1) | (fi.z >= midz);
             const unsigned short* lst = use_types ? tl + s_tbase[tau] : nullptr;
             const int len32 = use_types ? s_tbase[tau + 1] - s_tbase[tau] : M32;
@@ -549,7 +559,7 @@ __global__ void __launch_bounds__(kListWarps * 32, 4) k_list_v2(ListArgs a) {
                 const bool acc = (HALF ? (j > i) : (j != i && j >= 0)) && __double_as_longlong(r2) < rs2_bits;
                 const unsigned msk = __ballot_sync(0xffffffffu, acc);
                 const int pos = cursor + __popc(msk & lt);
-                if (acc && pos < cap) dst[pos] = j;
+                if (acc && pos < cap) dst[il_off(pos, skip)] = j;
                 cursor += __popc(msk);
             }
             if (lane == 0 && !DIRECT) {
@@ -992,7 +1002,7 @@ __global__ void __launch_bounds__(kListWarps * 32, LARGE ? 2 : 4) k_list_v4(List
                 if (r < nr) {
                     ri[r] = s_row[s_rowlist[u0 + r]];
                     const int64_t rr = __float_as_int(ri[r].w) - a.row_begin;
-                    dst[r] = a.out + (DIRECT ? a.ptr[rr] : rr * (int64_t)kRowCap);
+                    dst[r] = DIRECT ? a.out + a.ptr[rr] : padded_row(a.out, rr, a.il_skip);
                 }
             }
             const unsigned short* lst = tl + tau * kTL;
@@ -1023,8 +1033,8 @@ __global__ void __launch_bounds__(kListWarps * 32, LARGE ? 2 : 4) k_list_v4(List
                     const unsigned m1 = __ballot_sync(0xffffffffu, acc1);
                     const int p0 = cur[r] + __popc(m0 & lt);
                     const int p1 = cur[r] + __popc(m0) + __popc(m1 & lt);
-                    if (acc0 && (DIRECT || p0 < kRowCap)) dst[r][p0] = j0;
-                    if (acc1 && (DIRECT || p1 < kRowCap)) dst[r][p1] = j1;
+                    if (acc0 && (DIRECT || p0 < kRowCap)) dst[r][DIRECT ? p0 : il_off(p0, a.il_skip)] = j0;
+                    if (acc1 && (DIRECT || p1 < kRowCap)) dst[r][DIRECT ? p1 : il_off(p1, a.il_skip)] = j1;
                     cur[r] += __popc(m0) + __popc(m1);
                 }
             }
@@ -1108,9 +1118,10 @@ __global__ void __launch_bounds__(kListWarps * 32) k_list_fallback(ListArgs a) {
                 for (int k = m + lane; k < P; k += 32) buf[k] = INT_MAX;
                 __syncwarp();
                 warp_bitonic_sort(buf, P, lane);
-                int32_t* dst = DIRECT ? gdst : a.out + r * (int64_t)kRowCap;
+                int32_t* dst = DIRECT ? gdst : padded_row(a.out, r, a.il_skip);
                 const int lim = DIRECT ? cursor : min(m, kRowCap);
-                for (int k = lane; k < lim; k += 32) dst[k] = buf[k];
+                const int skip = DIRECT ? 0 : a.il_skip;
+                for (int k = lane; k < lim; k += 32) dst[il_off(k, skip)] = buf[k];
             } else if (lane == 0) {   // DIRECT, very long row: insertion sort in place
                 for (int x = 1; x < cursor; x++) {
                     int v = gdst[x], y = x - 1;
@@ -1397,6 +1408,7 @@ static ListArgs list_args(const double* q, const CellGrid& cg, double rs, int ha
     a.overflow_cells2 = a.overflow_cells + ncell_of(cg);
     a.setups = (const CellSetup*)(ws + W.off_setup);
     a.clamp = 0;
+    a.il_skip = 0;
     return a;
 }
 
@@ -1463,12 +1475,13 @@ static void launch_list_kernels(const ListArgs& a, const CellGrid& cg, int half,
 
 cudaError_t launch_list_pass1(const double* q, const CellGrid& cg, double rs, int half, int64_t row_begin,
                               int64_t row_end, int32_t* npart, int32_t* out, char* ws, const BuildWorkspace& W,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool interleaved) {
     cudaError_t e = set_list_attrs();
     if (e != cudaSuccess) return e;
     ListArgs a = list_args(q, cg, rs, half, row_begin, row_end, npart, nullptr,
                            out ? out : (int32_t*)(ws + W.off_scratch), ws, W);
     a.clamp = out != nullptr;   // the caller's padded list: counts clamped to the stride
+    a.il_skip = (out != nullptr && interleaved) ? kIlSkip : 0;
     e = cudaMemsetAsync(a.n_overflow, 0, 4 * sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     launch_list_kernels<0>(a, cg, half, s);
@@ -1494,13 +1507,18 @@ cudaError_t launch_list_pass2(const double* q, const CellGrid& cg, double rs, in
     return cudaGetLastError();
 }
 
-__global__ void k_padded_pointer(int64_t* ptr, int64_t rows) {
+__global__ void k_padded_pointer(int64_t* ptr, int64_t rows, int il) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= rows; r += (int64_t)gridDim.x * blockDim.x)
-        ptr[r] = r * (int64_t)kRowCap;
+        if (!il)
+            ptr[r] = r * (int64_t)kRowCap;
+        else if (r < rows)   // entry 0 of the row, flagged (row_decode)
+            ptr[r] = kIlBit | ((r >> 3) * (int64_t)(kIlRows * kRowCap) + (r & (kIlRows - 1)) * kIlGran);
+        else   // the padded extent
+            ptr[r] = ((rows + kIlRows - 1) / kIlRows) * (int64_t)(kIlRows * kRowCap);
 }
 
-cudaError_t launch_padded_pointer(int64_t* ptr, int64_t rows, cudaStream_t s) {
-    k_padded_pointer<<<grid_for(rows + 1, 256), 256, 0, s>>>(ptr, rows);
+cudaError_t launch_padded_pointer(int64_t* ptr, int64_t rows, cudaStream_t s, bool interleaved) {
+    k_padded_pointer<<<grid_for(rows + 1, 256), 256, 0, s>>>(ptr, rows, interleaved ? 1 : 0);
     g_launches++;
     return cudaGetLastError();
 }

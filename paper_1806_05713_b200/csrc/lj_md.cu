@@ -206,11 +206,13 @@ __global__ void __launch_bounds__(kThreads)
             const rec4 pi = p[i];
             ke += 0.5 * __dadd_rn(__dadd_rn(__dmul_rn(pi.x, pi.x), __dmul_rn(pi.y, pi.y)), __dmul_rn(pi.z, pi.z));
         }
-        const int32_t* __restrict__ l = list + ptr[r];
+        int skip;
+        const int32_t* __restrict__ l = row_decode(list, ptr[r], skip);
         const int n = npart[r];
         for (int k = g; k < n; k += G) {
-            LJ_CHECK_THAT(l[k] >= 0 && l[k] < n_atoms);
-            const rec4 qj = load_rec(q, __ldg(l + k));
+            const int j = __ldg(l + il_off(k, skip));
+            LJ_CHECK_THAT(j >= 0 && j < n_atoms);
+            const rec4 qj = load_rec(q, j);
             double dx = qj.x - qi.x, dy = qj.y - qi.y, dz = qj.z - qi.z;
             if (L > 0.0) {
                 dx = dx > halfL ? dx - L : (dx < -halfL ? dx + L : dx);
@@ -246,10 +248,11 @@ __global__ void k_list_interior(int64_t row_begin, int64_t row_end, const int32_
     for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < row_end - row_begin;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int n = npart[r];
-        const int32_t* l = list + ptr[r];
+        int skip;
+        const int32_t* l = row_decode(list, ptr[r], skip);
         bool out_of_slab = false;
         for (int k = lane; k < n; k += 32) {
-            const int j = l[k];
+            const int j = l[il_off(k, skip)];
             out_of_slab |= j < row_begin || j >= row_end;
         }
         if (__any_sync(0xffffffffu, out_of_slab) && lane == 0) {
@@ -284,11 +287,12 @@ __global__ void k_partner_ranges(int64_t row_begin, int64_t row_end, const int32
     for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < row_end - row_begin;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int n = npart[r];
-        const int32_t* l = list + ptr[r];
+        int skip;
+        const int32_t* l = row_decode(list, ptr[r], skip);
         int prev_owner = -1;   // owner of the entry before this chunk (warp-uniform)
         for (int k0 = 0; k0 < n; k0 += 32) {
             const int k = k0 + lane;
-            const long long j = k < n ? l[k] : -1;
+            const long long j = k < n ? l[il_off(k, skip)] : -1;
             int own = -1;
             if (k < n) {
                 int lo = 0, hi = P;   // owner: largest s with s_b[s] <= j

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblj.so")
 
 LJ_OK, LJ_ERR_ARG, LJ_ERR_CAPACITY, LJ_ERR_CUDA, LJ_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
-LJ_LIST_PADDED, LJ_LIST_DEFERRED, LJ_PADDED_ROW_STRIDE = 1, 2, 196   # include/liblj.h
+LJ_LIST_PADDED, LJ_LIST_DEFERRED, LJ_LIST_INTERLEAVED, LJ_PADDED_ROW_STRIDE = 1, 2, 4, 196   # include/liblj.h
 LJ_LANES_IDXV = 1 << 16   # include/liblj.h: index vector loads (lanes_per_row = G | V << 8 | LJ_LANES_IDXV)
 LAYOUTS = {"aos4": 0, "soa": 1, "aos3": 2, "aos8": 3}                    # LJ_LAYOUT_*
 RECIPROCALS = {"newton3": 0, "newton2": 1, "approx": 2, "ieee": 3}       # LJ_RCP_*
@@ -70,7 +70,7 @@ class MDGraphDesc(ctypes.Structure):
                 ("sorted_list", ctypes.c_void_p), ("capacity", ctypes.c_int64), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t), ("disp", ctypes.c_void_p), ("n_interactions", ctypes.c_void_p),
                 ("status", ctypes.c_void_p), ("reorder", ctypes.c_int), ("steps", ctypes.c_int),
-                ("energy_every", ctypes.c_int), ("energies", ctypes.c_void_p)]
+                ("energy_every", ctypes.c_int), ("energies", ctypes.c_void_p), ("interleaved", ctypes.c_int)]
 
 
 class MDRebuildDesc(ctypes.Structure):
@@ -82,7 +82,8 @@ class MDRebuildDesc(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_size_t), ("disp", ctypes.c_void_p), ("disp_count", ctypes.c_int),
                 ("disp_stride", ctypes.c_int64), ("status", ctypes.c_void_p), ("reorder", ctypes.c_int),
                 ("q_alt", ctypes.c_void_p), ("p", ctypes.c_void_p), ("p_alt", ctypes.c_void_p),
-                ("perm", ctypes.c_void_p), ("p_peers", ctypes.c_void_p), ("n_own", ctypes.c_int64)]
+                ("perm", ctypes.c_void_p), ("p_peers", ctypes.c_void_p), ("n_own", ctypes.c_int64),
+                ("interleaved", ctypes.c_int)]
 
 
 _lib = None
@@ -226,7 +227,8 @@ class CSRList:
     row_begin: int
     row_end: int
     half: bool
-    padded: bool = False   # LJ_LIST_PADDED layout (rows at a fixed stride)
+    padded: bool = False        # LJ_LIST_PADDED layout (rows at a fixed stride)
+    interleaved: bool = False   # LJ_LIST_INTERLEAVED (padded rows in blocks of 8, entries interleaved by 4)
 
     @property
     def rows(self):
@@ -239,7 +241,23 @@ class CSRList:
             raise ValueError(f"rows_view: [{a},{b}) not within [{self.row_begin},{self.row_end})")
         o = a - self.row_begin
         return CSRList(self.number_of_partners[o:o + (b - a)], self.pointer[o:], self.sorted_list, self.n_entries,
-                       a, b, self.half, self.padded)
+                       a, b, self.half, self.padded, self.interleaved)
+
+    def padded_rows(self) -> torch.Tensor:
+        """The rows of a padded list (either layout) as a [rows, LJ_PADDED_ROW_STRIDE] int32
+        tensor in row-major order (entries past number_of_partners undefined).  For tests and
+        tools; a view for the plain padded layout, a copy for the interleaved one."""
+        if not self.padded:
+            raise ValueError("padded_rows: not a padded list")
+        base = int(self.pointer[0].item()) & ((1 << 62) - 1)
+        R, S = self.rows, LJ_PADDED_ROW_STRIDE
+        if not self.interleaved:
+            return self.sorted_list[base:base + R * S].view(R, S)
+        if base % (8 * S) != 0:
+            raise ValueError("padded_rows: an interleaved list view must start at a block of 8 rows")
+        nb = (R + 7) // 8
+        blk = self.sorted_list[base:base + nb * 8 * S].view(nb, S // 4, 8, 4)
+        return blk.permute(0, 2, 1, 3).reshape(nb * 8, S)[:R]
 
 
 class ListBuilder:
@@ -247,7 +265,7 @@ class ListBuilder:
 
     def __init__(self, n: int, g: Geom, half: bool, row_begin: int = 0, row_end: int | None = None,
                  device=None, headroom: float = 1.15, initial_per_row: int = 0, padded: bool = False,
-                 deferred: bool = False):
+                 deferred: bool = False, interleaved: bool = False):
         self.n, self.g, self.half = int(n), g, bool(half)
         self.row_begin = int(row_begin)
         self.row_end = int(n if row_end is None else row_end)
@@ -260,9 +278,14 @@ class ListBuilder:
         self.npart = torch.empty(max(rows, 1), dtype=torch.int32, device=self.device)
         self.pointer = torch.empty(rows + 1, dtype=torch.int64, device=self.device)
         self.padded = padded
+        self.interleaved = bool(interleaved) and padded   # LJ_LIST_INTERLEAVED (padded layouts only)
+        alloc_rows = rows
         if padded:
             initial_per_row = LJ_PADDED_ROW_STRIDE
-        self.sorted_list = torch.empty(max(int(rows * initial_per_row), 1), dtype=torch.int32, device=self.device)
+            if self.interleaved:
+                alloc_rows = (rows + 7) // 8 * 8
+        self.sorted_list = torch.empty(max(int(alloc_rows * initial_per_row), 1), dtype=torch.int32,
+                                       device=self.device)
         self.rebuilds = 0
         # LJ_LIST_DEFERRED (padded layout only): the build does not synchronise; its status
         # lands in pinned memory and is checked by resolve() after a later synchronisation
@@ -282,7 +305,8 @@ class ListBuilder:
         return int(self.npart[:rows].max().item()) if rows > 0 else 0
 
     def _flags(self):
-        return (LJ_LIST_PADDED if self.padded else 0) | (LJ_LIST_DEFERRED if self.deferred and self.padded else 0)
+        return ((LJ_LIST_PADDED if self.padded else 0) | (LJ_LIST_DEFERRED if self.deferred and self.padded else 0)
+                | (LJ_LIST_INTERLEAVED if self.interleaved and self.padded else 0))
 
     def build(self, q: torch.Tensor) -> CSRList:
         _rec(q, "q")
@@ -339,7 +363,7 @@ class ListBuilder:
             self.rebuilds += 1
             rows = self.row_end - self.row_begin
             lst = CSRList(self.npart[:rows], self.pointer, self.sorted_list, -1, self.row_begin, self.row_end,
-                          self.half, True)
+                          self.half, True, self.interleaved)
             self._unresolved = lst
             return lst
         ne = ctypes.c_int64(0)
@@ -347,6 +371,7 @@ class ListBuilder:
             st = call(ctypes.byref(ne))
             if st == LJ_ERR_UNSUPPORTED and self.padded:   # a row longer than the stride: compact from now on
                 self.padded = False
+                self.interleaved = False
                 continue
             if st == LJ_ERR_CAPACITY:
                 cap = int(ne.value * self.headroom) + 1024
@@ -359,7 +384,7 @@ class ListBuilder:
         self.rebuilds += 1
         rows = self.row_end - self.row_begin
         return CSRList(self.npart[:rows], self.pointer, self.sorted_list, int(ne.value), self.row_begin,
-                       self.row_end, self.half, self.padded)
+                       self.row_end, self.half, self.padded, self.interleaved)
 
 
 def build_list(q: torch.Tensor, g: Geom, half: bool, row_begin: int = 0, row_end: int | None = None) -> CSRList:
@@ -429,7 +454,7 @@ class MDGraph:
                         _ptr(builder.sorted_list).value, builder.sorted_list.numel(), _ptr(builder.workspace).value,
                         builder.workspace.numel(), _ptr(disp).value, _ptr(counter).value if counter is not None
                         else None, _ptr(status).value, int(bool(reorder)), self.steps, int(energy_every),
-                        _ptr(energies).value if energies is not None else None)
+                        _ptr(energies).value if energies is not None else None, int(builder.interleaved))
         h = ctypes.c_void_p()
         _check(load().lj_md_graph_create(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
@@ -485,7 +510,7 @@ def md_capture_rebuild(q: torch.Tensor, q_ref: torch.Tensor, g: Geom, builder: "
                       builder.sorted_list.numel(), _ptr(builder.workspace).value, builder.workspace.numel(),
                       _ptr(disp).value, int(disp_count), int(disp_stride), _ptr(status).value,
                       int(resort is not None), _addr(r.get("q_alt")), _addr(r.get("p")), _addr(r.get("p_alt")),
-                      _addr(r.get("perm")), _addr(r.get("p_peers")), int(r.get("n_own", 0)))
+                      _addr(r.get("perm")), _addr(r.get("p_peers")), int(r.get("n_own", 0)), int(builder.interleaved))
     k = ctypes.c_longlong(0)
     _check(load().lj_md_capture_rebuild(ctypes.byref(d), _stream(), ctypes.byref(k)))
     return k.value

@@ -44,7 +44,7 @@ def row_range(n: int, rank: int, world: int) -> tuple[int, int]:
 class LibBackend:
     """liblj.so on the current CUDA device."""
 
-    def __init__(self, n, g: lj.Geom, row_begin, row_end, device, half=False, deferred=True):
+    def __init__(self, n, g: lj.Geom, row_begin, row_end, device, half=False, deferred=True, interleaved=None):
         lj.load()
         self.device = torch.device(device)
         self.n, self.g = n, g
@@ -54,8 +54,12 @@ class LibBackend:
         # min(count, stride) and raises the overflow flag, which resolve() / StepGraph.finish()
         # turn into LJ_ERR_UNSUPPORTED.
         self._want_deferred = bool(deferred)
+        # The interleaved padded layout (LJ_LIST_INTERLEAVED: the force kernel's index loads are
+        # one 128-B line per warp) unless LJ_LIST_INTERLEAVE=0 (A/B measurements).
+        if interleaved is None:
+            interleaved = os.environ.get("LJ_LIST_INTERLEAVE", "1") != "0"
         self.builder = lj.ListBuilder(n, g, half, row_begin, row_end, device=self.device, padded=True,
-                                      deferred=False)
+                                      deferred=False, interleaved=interleaved)
         self.perm = None   # scratch of the re-sorting rebuild (allocated on first use)
 
     ROW_MARGIN = 24

@@ -39,8 +39,8 @@ def _windows(n, seed):
     return [(0, WIN), (n // 2 - WIN // 2, n // 2 + WIN // 2), (a, a + WIN), (n - WIN, n)]
 
 
-@pytest.mark.parametrize("cfg", [4, 5])
-def test_fullsize_sampled_parity(lj, cfg):
+@pytest.mark.parametrize("cfg,interleaved", [(4, False), (4, True), (5, True)])
+def test_fullsize_sampled_parity(lj, cfg, interleaved):
     dev = torch.device("cuda:0")
     w = lj_inputs.config(cfg)
     perm = oracle.cell_order(w.q, w.L, w.rs)          # the bench's storage order
@@ -49,10 +49,10 @@ def test_fullsize_sampled_parity(lj, cfg):
     g = lj.geom(w.L, w.rc, w.rs)
     q = lj.pack_aos4(torch.from_numpy(qn).to(dev))
     p = lj.pack_aos4(torch.from_numpy(pn).to(dev))
-    b = lj.ListBuilder(w.n, g, False, device=dev, padded=True)
+    b = lj.ListBuilder(w.n, g, False, device=dev, padded=True, interleaved=interleaved)
     gl = b.build(q)
-    assert gl.padded, "the bench's layout: padded rows"
-    stride = lj.LJ_PADDED_ROW_STRIDE
+    assert gl.padded and gl.interleaved == interleaved, "the bench's layout: padded (interleaved) rows"
+    prow = gl.padded_rows()
     npart = gl.number_of_partners.cpu().numpy()
     assert int(npart.sum()) == gl.n_entries
     # one force step, default launch configuration (as bench.py)
@@ -65,7 +65,7 @@ def test_fullsize_sampled_parity(lj, cfg):
     for (a, e) in _windows(w.n, cfg):
         ol = oracle.list_cells(qn, w.L, w.rs, False, a, e)
         assert np.array_equal(npart[a:e], ol.number_of_partners), f"row lengths differ in [{a},{e})"
-        rows = gl.sorted_list[a * stride:e * stride].view(e - a, stride).cpu().numpy()
+        rows = prow[a:e].cpu().numpy()
         for r in range(a, e):
             assert np.array_equal(rows[r - a, :npart[r]], ol.row(r - a)), f"row {r}"
         ref = oracle.force_step(qn, pn, w.L, w.rc, w.dt, ol)
@@ -82,14 +82,14 @@ def test_fullsize_half_list_sampled(lj):
     qn = np.ascontiguousarray(w.q[perm])
     g = lj.geom(w.L, w.rc, w.rs)
     q = lj.pack_aos4(torch.from_numpy(qn).to(dev))
-    gl = lj.ListBuilder(w.n, g, True, device=dev, padded=True).build(q)
-    stride = lj.LJ_PADDED_ROW_STRIDE
+    gl = lj.ListBuilder(w.n, g, True, device=dev, padded=True, interleaved=True).build(q)
+    prow = gl.padded_rows()
     npart = gl.number_of_partners.cpu().numpy()
     assert int(npart.sum()) == gl.n_entries
     for (a, e) in _windows(w.n, 44):
         ol = oracle.list_cells(qn, w.L, w.rs, True, a, e)
         assert np.array_equal(npart[a:e], ol.number_of_partners)
-        rows = gl.sorted_list[a * stride:e * stride].view(e - a, stride).cpu().numpy()
+        rows = prow[a:e].cpu().numpy()
         for r in range(a, e):
             assert np.array_equal(rows[r - a, :npart[r]], ol.row(r - a)), f"row {r}"
 
@@ -117,11 +117,12 @@ def test_fullsize_snapshot_parity_after_md_rebuild(lj):
     ids = np.sort(sim.atom_ids().cpu().numpy())
     assert np.array_equal(ids, np.arange(w.n))
     lst = sim.lst
-    stride = lj.LJ_PADDED_ROW_STRIDE
+    assert lst.interleaved, "the bench's layout"
+    prow = lst.padded_rows()
     npart = lst.number_of_partners.cpu().numpy()
     for (a, e) in _windows(w.n, 13):
         ol = oracle.list_cells(qs, w.L, w.rs, False, a, e)
         assert np.array_equal(npart[a:e], ol.number_of_partners)
-        rows = lst.sorted_list[a * stride:e * stride].view(e - a, stride).cpu().numpy()
+        rows = prow[a:e].cpu().numpy()
         for r in range(a, e):
             assert np.array_equal(rows[r - a, :npart[r]], ol.row(r - a)), f"row {r}"

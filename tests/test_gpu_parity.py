@@ -407,6 +407,73 @@ def test_padded_layout_same_rows(lj, dev, systems, cfg, half):
         assert torch.equal(pa, pb)
 
 
+IL_LANES = [0, 1 | 512, 2 | 768, 4 | 512, 4 | 768, 4 | 1024, 8 | 512, 8 | 768, 16 | 512, 32 | 768,
+            4 | 512 | (1 << 16), 4 | 1024 | (1 << 16), 8 | 512 | (1 << 16), 2 | 1024 | (1 << 16)]
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+@pytest.mark.parametrize("half,rows", [(False, None), (True, None), (False, (123, 3001)), (False, (8, 4000))])
+def test_interleaved_layout(lj, dev, systems, cfg, half, rows):
+    """LJ_LIST_INTERLEAVED (include/liblj.h): pointer[r] = bit 62 | (r//8)*8*S + (r%8)*4,
+    entry e of row r at pointer + e + 28*(e//4), pointer[rows] = the padded extent; the rows
+    are the oracle's (read from that definition on the host); and every consumer -- the force
+    kernel for every lanes / unroll / index-vector variant, the ordered kernel, energy,
+    interior rows, partner ranges, the half-cell kernel -- gives the same result on the
+    interleaved list as on the plain padded one (bit-identical where deterministic)."""
+    w = systems[cfg]
+    rb, re_ = rows or (0, w.n)
+    g = lj.geom(w.L, w.rc, w.rs)
+    q = to_dev(w.q, dev)
+    plain = lj.ListBuilder(w.n, g, half, rb, re_, device=dev, padded=True).build(q)
+    bil = lj.ListBuilder(w.n, g, half, rb, re_, device=dev, padded=True, interleaved=True)
+    il = bil.build(q)
+    assert il.interleaved and not plain.interleaved and il.n_entries == plain.n_entries
+    R, S = re_ - rb, lj.LJ_PADDED_ROW_STRIDE
+    r = np.arange(R, dtype=np.int64)
+    ptr = il.pointer.cpu().numpy()
+    assert np.array_equal(ptr[:R], (1 << 62) | ((r // 8) * 8 * S + (r % 8) * 4))
+    assert ptr[R] == (R + 7) // 8 * 8 * S
+    sl = il.sorted_list.cpu().numpy()
+    npart = il.number_of_partners.cpu().numpy()
+    ol = oracle.list_cells(w.q, w.L, w.rs, half, rb, re_)
+    assert np.array_equal(npart, ol.number_of_partners)
+    for rr in list(range(0, R, 37)) + [R - 1]:
+        e = np.arange(npart[rr])
+        assert np.array_equal(sl[(int(ptr[rr]) & ((1 << 62) - 1)) + e + 28 * (e // 4)], ol.row(rr)), rr
+    v = torch.arange(S, device=dev)[None, :] < il.number_of_partners[:, None]
+    assert torch.equal(il.padded_rows()[v], plain.padded_rows()[v])
+    p0 = np.random.default_rng(3).normal(0, 1, (w.n, 3))
+    ref, Sab, _ = oracle_force(w, p0, half) if rows is None else (None, None, None)
+    for lanes in IL_LANES:
+        pa, pb = to_dev(p0, dev), to_dev(p0, dev)
+        ca, cb = (torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(2))
+        lj.force_step(q, pa, g, w.dt, plain, lanes_per_row=lanes, n_interactions=ca)
+        lj.force_step(q, pb, g, w.dt, il, lanes_per_row=lanes, n_interactions=cb)
+        assert int(ca.item()) == int(cb.item()), lanes
+        if half:   # fp64 REDs: the order of the partner contributions is not deterministic
+            assert oracle.parity_error(from_dev(pb), ref, Sab) <= TOL, lanes
+        else:
+            assert torch.equal(pa, pb), lanes
+    if not half:
+        pa, pb = to_dev(p0, dev), to_dev(p0, dev)
+        lj.force_step(q, pa, g, w.dt, plain, ordered=True)
+        lj.force_step(q, pb, g, w.dt, il, ordered=True)
+        assert torch.equal(pa, pb)
+        assert lj.list_interior(plain) == lj.list_interior(il)
+        bounds = [w.n * s // 4 for s in range(4)] + [w.n]
+        assert lj.list_partner_ranges(plain, bounds) == lj.list_partner_ranges(il, bounds)
+        sink = torch.zeros(4, dtype=torch.float64, device=dev)
+        lj.gather_probe(q, il, 0, sink)
+    pt = to_dev(p0, dev)
+    ea = lj.energy(q, pt, g, plain).cpu().numpy()
+    eb = lj.energy(q, pt, g, il).cpu().numpy()
+    assert np.allclose(ea, eb, rtol=1e-13, atol=0.0)
+    if half and rows is None:   # the per-cell shared-memory kernel reads the same rows
+        pc = to_dev(p0, dev)
+        lj.force_step_half_cells(q, pc, g, w.dt, il, bil.cell_starts())
+        assert oracle.parity_error(from_dev(pc), ref, Sab) <= TOL
+
+
 def test_padded_layout_falls_back_on_long_rows(lj, dev):
     """Rows longer than the stride (dense gas) -> UNSUPPORTED -> the builder switches to compact."""
     q = lj_inputs.random_gas(5000, 9.9, 4)
@@ -418,7 +485,7 @@ def test_padded_layout_falls_back_on_long_rows(lj, dev):
 
 
 @pytest.mark.parametrize("padded,rows", [(True, (0, 4000)), (False, (0, 4000)), (True, (1000, 3000)),
-                                         (False, (123, 456))])
+                                         (False, (123, 456)), ("il", (0, 4000)), ("il", (123, 3001))])
 def test_rebuild_fused_equals_steps(lj, dev, systems, padded, rows):
     """lj_rebuild == lj_wrap + lj_cell_order + lj_permute_rows (q, p, q_ref) +
     lj_build_list_ex on the permuted system, bit for bit, for drifted (unwrapped)
@@ -436,20 +503,29 @@ def test_rebuild_fused_equals_steps(lj, dev, systems, padded, rows):
     lj.wrap(qa, w.L)
     perm_a = lj.cell_order(qa, g)
     qa2, pa2 = lj.permute_rows(qa, perm_a), lj.permute_rows(pa, perm_a)
-    la = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=padded).build(qa2)
+    il = padded == "il"
+    padded = bool(padded)
+    la = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=padded, interleaved=il).build(qa2)
     # fused
     qb = to_dev(q_np, dev, pad)
     pb = to_dev(p_np, dev, pad)
     qb2, pb2, qref = torch.empty_like(qb), torch.empty_like(pb), torch.empty_like(qb)
     perm_b = torch.empty(w.n, dtype=torch.int64, device=dev)
-    lb = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=padded).rebuild(qb, pb, qb2, pb2, qref, perm_b)
+    lb = lj.ListBuilder(w.n, g, False, rb, re_, device=dev, padded=padded,
+                        interleaved=il).rebuild(qb, pb, qb2, pb2, qref, perm_b)
     assert torch.equal(qa, qb)          # wrapped in place
     assert torch.equal(perm_a, perm_b)
     assert torch.equal(qa2, qb2) and torch.equal(pa2, pb2) and torch.equal(qa2, qref)
     assert la.n_entries == lb.n_entries
     assert torch.equal(la.number_of_partners, lb.number_of_partners) and torch.equal(la.pointer, lb.pointer)
     nrow = re_ - rb
-    for r in range(0, nrow, max(1, nrow // 50)):   # valid entries of sampled rows (padded rows have gaps)
+    if padded:
+        assert la.interleaved == lb.interleaved == il
+        v = torch.arange(lj.LJ_PADDED_ROW_STRIDE, device=dev)[None, :] < la.number_of_partners[:, None]
+        assert torch.equal(la.padded_rows()[v], lb.padded_rows()[v])
+    for r in range(0, nrow, max(1, nrow // 50)):   # valid entries of sampled rows (compact)
+        if padded:
+            break
         b0, n0 = int(la.pointer[r]), int(la.number_of_partners[r])
         assert torch.equal(la.sorted_list[b0:b0 + n0], lb.sorted_list[b0:b0 + n0])
     # the permutation is the oracle's cell order of the wrapped positions
@@ -668,14 +744,15 @@ def test_degenerate_systems_step(lj, dev, n):
     assert torch.equal(q, q2)
 
 
-def test_deferred_padded_build(lj, dev, systems):
+@pytest.mark.parametrize("il", [False, True])
+def test_deferred_padded_build(lj, dev, systems, il):
     """LJ_LIST_DEFERRED: the same list as the synchronous padded build, n_entries
     resolved after a synchronisation; a row over the stride is reported by resolve()."""
     w = systems[3]
     g = lj.geom(w.L, w.rc, w.rs)
     q = to_dev(w.q, dev)
-    ref = lj.ListBuilder(w.n, g, False, device=dev, padded=True).build(q)
-    b = lj.ListBuilder(w.n, g, False, device=dev, padded=True, deferred=True)
+    ref = lj.ListBuilder(w.n, g, False, device=dev, padded=True, interleaved=il).build(q)
+    b = lj.ListBuilder(w.n, g, False, device=dev, padded=True, deferred=True, interleaved=il)
     gl = b.build(q)
     assert gl.n_entries == -1
     torch.cuda.synchronize()
@@ -683,10 +760,9 @@ def test_deferred_padded_build(lj, dev, systems):
     assert gl.n_entries == ref.n_entries
     assert torch.equal(gl.number_of_partners, ref.number_of_partners)
     assert torch.equal(gl.pointer, ref.pointer)
-    n = w.n * lj.LJ_PADDED_ROW_STRIDE
-    v = torch.arange(n, device=dev) % lj.LJ_PADDED_ROW_STRIDE < gl.number_of_partners.repeat_interleave(
-        lj.LJ_PADDED_ROW_STRIDE)
-    assert torch.equal(gl.sorted_list[:n][v], ref.sorted_list[:n][v])
+    assert gl.interleaved == ref.interleaved == il
+    v = torch.arange(lj.LJ_PADDED_ROW_STRIDE, device=dev)[None, :] < gl.number_of_partners[:, None]
+    assert torch.equal(gl.padded_rows()[v], ref.padded_rows()[v])
     # a second deferred build before resolving: the builder synchronises and resolves the first
     gl2 = b.build(q)
     assert gl.n_entries == ref.n_entries
@@ -702,7 +778,8 @@ def test_deferred_padded_build(lj, dev, systems):
         bd.resolve()
 
 
-def test_overflowed_padded_list_stays_in_bounds(lj, dev):
+@pytest.mark.parametrize("il", [False, True])
+def test_overflowed_padded_list_stays_in_bounds(lj, dev, il):
     """a padded row over the stride stores min(count, stride) in
     number_of_partners, so a force step that runs before the overflow is
     noticed (deferred build, graph rebuild) reads inside the list; the overflow
@@ -710,7 +787,7 @@ def test_overflowed_padded_list_stays_in_bounds(lj, dev):
     S = lj.LJ_PADDED_ROW_STRIDE
     qg = to_dev(lj_inputs.random_gas(5000, 9.9, 4), dev)
     g = lj.geom(9.9, 3.0, 3.3)
-    bd = lj.ListBuilder(5000, g, False, device=dev, padded=True, deferred=True)
+    bd = lj.ListBuilder(5000, g, False, device=dev, padded=True, deferred=True, interleaved=il)
     lst = bd.build(qg)
     p = to_dev(np.zeros((5000, 3)), dev)
     lj.force_step(qg, p, g, 0.0, lst)             # before resolve(): must not fault
@@ -724,9 +801,9 @@ def test_overflowed_padded_list_stays_in_bounds(lj, dev):
     gg = lj.geom(L, 3.0, 3.3)
     q = to_dev(q0, dev)
     pm = to_dev(np.zeros((n, 3)), dev)
-    b = lj.ListBuilder(n, gg, False, device=dev, padded=True)
+    b = lj.ListBuilder(n, gg, False, device=dev, padded=True, interleaved=il)
     b.build(q)
-    assert b.padded
+    assert b.padded and b.interleaved == il
     q2 = q0.copy()
     q2[:400] = 10.0 + np.random.default_rng(1).uniform(-1.5, 1.5, (400, 3))   # ~28 atoms per unit volume
     q.copy_(to_dev(q2, dev))
@@ -755,16 +832,15 @@ def test_list_storage_drifted_from_cell_order(lj, dev, systems, drift, half):
     rng = np.random.default_rng(int(drift * 100) + half)
     q = lj_inputs.wrap_into_box(w.q + rng.uniform(-drift, drift, w.q.shape), w.L)
     g = lj.geom(w.L, w.rc, w.rs)
-    for padded in (False, True):
-        b = lj.ListBuilder(w.n, g, half, device=dev, padded=padded)
+    for padded, il in ((False, False), (True, False), (True, True)):
+        b = lj.ListBuilder(w.n, g, half, device=dev, padded=padded, interleaved=il)
         gl = b.build(to_dev(q, dev))
         ol = oracle.list_cells(q, w.L, w.rs, half)
         if padded:
             n_e = ol.n_entries
-            assert gl.n_entries == n_e
+            assert gl.n_entries == n_e and gl.interleaved == il
             assert np.array_equal(gl.number_of_partners.cpu().numpy(), ol.number_of_partners)
-            S = lj.LJ_PADDED_ROW_STRIDE
-            rows = gl.sorted_list[: w.n * S].view(w.n, S).cpu().numpy()
+            rows = gl.padded_rows().cpu().numpy()
             for i in range(0, w.n, 97):   # sampled rows: identical, ascending
                 k = ol.number_of_partners[i]
                 assert np.array_equal(rows[i, :k], ol.sorted_list[ol.pointer[i]:ol.pointer[i] + k])

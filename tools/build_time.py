@@ -33,14 +33,14 @@ def main():
         q = lj.pack_aos4(torch.from_numpy(w.q).to(dev))
         perm = lj.cell_order(q, g)
         q = lj.permute_rows(q, perm)
-        for padded in (False, True):
+        for padded in (False, True, "il"):
             for half in ((False, True) if c < 4 else (False,)):
-                b = lj.ListBuilder(w.n, g, half, device=dev, padded=padded)
+                b = lj.ListBuilder(w.n, g, half, device=dev, padded=bool(padded), interleaved=padded == "il")
                 lst = b.build(q)
                 ms = timeit(lambda: b.build(q))
                 print(json.dumps(dict(cfg=c, half=half, padded=padded, what="build", ms=round(ms, 4),
                                       entries=lst.n_entries)), flush=True)
-                if padded and not half:
+                if padded and not half:   # (the interleaved layout: also the force step on it)
                     # lj_rebuild (wrap + cell-order permutation + list): the MD path's builder
                     q_out, p_in = torch.empty_like(q), torch.zeros_like(q)
                     p_out, perm = torch.empty_like(q), torch.empty(w.n, dtype=torch.int64, device=dev)
@@ -48,6 +48,11 @@ def main():
                     ms = timeit(lambda: b.rebuild(q, p_in, q_out, p_out, None, perm))
                     print(json.dumps(dict(cfg=c, half=half, padded=padded, what="rebuild", ms=round(ms, 4),
                                           entries=lst.n_entries)), flush=True)
+                    for lanes in (0, 4 | 512, 8 | 512):
+                        ms = min(timeit(lambda: lj.force_step(q_out, p_out, g, w.dt, lst, lanes_per_row=lanes),
+                                        reps=20) for _ in range(3))
+                        print(json.dumps(dict(cfg=c, padded=padded, what="force", lanes=lanes, ms=round(ms, 4),
+                                              entries=lst.n_entries)), flush=True)
                     del q_out, p_in, p_out, perm
                 del b, lst
                 torch.cuda.empty_cache()
