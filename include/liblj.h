@@ -431,6 +431,12 @@ lj_status lj_md_capture_rebuild(const lj_md_rebuild_desc *d, void *stream, long 
  * rank's own momenta into the buffer its peers read at a re-sorting rebuild. */
 lj_status lj_copy_records(const double *src, double *dst, int64_t n, void *stream);
 
+/* bytes from src to dst, stream-ordered, either side device or page-locked host
+ * memory (cudaMemcpyAsync, direction from the addresses): the per-step state
+ * copies of the end-to-end step graph (md.LeapfrogMD.graph_host_io), capturable
+ * into a CUDA graph.  Asynchronous. */
+lj_status lj_copy_bytes(void *dst, const void *src, size_t bytes, void *stream);
+
 /* The multi-rank re-sort on its own (lj_rebuild's cell pass without the list):
  * q (n records, replicated) is wrapped in place, perm[new] = old is the stable
  * cell order, q_out = q permuted, q_ref = q_out (if not NULL), and for the own

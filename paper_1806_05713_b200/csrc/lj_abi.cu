@@ -830,6 +830,13 @@ lj_status lj_copy_records(const double* src, double* dst, int64_t n, void* strea
     return LJ_OK;
 }
 
+lj_status lj_copy_bytes(void* dst, const void* src, size_t bytes, void* stream) {
+    if (bytes > 0 && (!src || !dst)) return fail(LJ_ERR_ARG, "copy_bytes: null pointer");
+    if (bytes == 0 || src == dst) return LJ_OK;
+    LJ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream), "lj_copy_bytes");
+    return LJ_OK;
+}
+
 lj_status lj_permute_rows_peers(double* q, double* q_out, double* q_ref, double* p_out,
                                 const double* const* p_peers, int64_t n_own, int64_t own_lo, int64_t own_hi,
                                 int64_t* perm, int64_t n, lj_geom g, void* workspace, size_t workspace_bytes,

@@ -31,7 +31,7 @@ EXPORTS = (
     "lj_gather_probe",
     "lj_list_cell_starts", "lj_force_step_half_cells",
     "lj_md_graph_create", "lj_md_graph_launch", "lj_md_graph_force_ms", "lj_md_graph_kernels", "lj_md_graph_destroy",
-    "lj_md_capture_rebuild", "lj_copy_records", "lj_permute_rows_peers", "lj_publish_scalar",
+    "lj_md_capture_rebuild", "lj_copy_records", "lj_copy_bytes", "lj_permute_rows_peers", "lj_publish_scalar",
     "lj_list_interior", "lj_list_partner_ranges", "lj_integrate", "lj_integrate_displacement",
     "lj_integrate_push", "lj_ipc_get_handle", "lj_ipc_open", "lj_ipc_close",
     "lj_wrap",
@@ -125,6 +125,7 @@ def load() -> ctypes.CDLL:
         "lj_md_capture_rebuild": (st, [ctypes.POINTER(MDRebuildDesc), vp, ctypes.POINTER(ctypes.c_longlong)]),
         "lj_publish_scalar": (st, [vp, vp, vp]),
         "lj_copy_records": (st, [vp, vp, i64, vp]),
+        "lj_copy_bytes": (st, [vp, vp, sz, vp]),
         "lj_permute_rows_peers": (st, [vp, vp, vp, vp, vp, i64, i64, i64, vp, i64, Geom, vp, sz, vp]),
         "lj_md_graph_force_ms": (st, [vp, ctypes.POINTER(ctypes.c_float), i32]),
         "lj_md_graph_kernels": (st, [vp, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
@@ -523,6 +524,18 @@ def copy_records(src: torch.Tensor, dst: torch.Tensor) -> None:
     if src.shape[0] != dst.shape[0]:
         raise ValueError("copy_records: shapes differ")
     _check(load().lj_copy_records(_ptr(src), _ptr(dst), src.shape[0], _stream()))
+
+
+def copy_bytes(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """lj_copy_bytes: dst[:] = src[:] (same dtype and element count; device or pinned host
+    memory on either side; stream-ordered on the current stream; capturable)."""
+    if dst.dtype != src.dtype or dst.numel() != src.numel() or not (dst.is_contiguous() and src.is_contiguous()):
+        raise ValueError("copy_bytes: contiguous tensors of the same dtype and size")
+    for t in (dst, src):
+        if not (t.is_cuda or t.is_pinned()):
+            raise ValueError("copy_bytes: device or pinned host tensors")
+    _check(load().lj_copy_bytes(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(src.data_ptr()),
+                                dst.numel() * dst.element_size(), _stream()))
 
 
 def permute_rows_peers(q: torch.Tensor, q_out: torch.Tensor, q_ref: torch.Tensor | None, p_out: torch.Tensor,

@@ -645,6 +645,110 @@ class LeapfrogMD:
         per_step_total = lj.launch_count() - l0 - kpr * steps
         return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr), status)
 
+    def graph_host_io(self, steps: int, q_host: torch.Tensor, p_host: torch.Tensor, chunks: int = 8,
+                      chunk_min_rows: int = 1 << 20) -> "StepGraph":
+        """The next `steps` leapfrog steps as ONE CUDA graph in which the state round-trips
+        through the caller's page-locked host arrays q_host / p_host ((n, 3) float64, storage
+        order) every step -- the end-to-end measurement of bench.py, one rank.  Per step: the
+        H2D copies of p and q in `chunks` row chunks on a copy stream (lj_copy_bytes), packed
+        into the records (lj_pack_aos4); the device-side bookkeeping decision on the previous
+        drift's displacement with the conditional re-sorting rebuild (lj_md_capture_rebuild);
+        the kick per row chunk, each chunk's momenta unpacked and sent back (D2H) at once on a
+        second copy stream; the drift + displacement; q unpacked and sent back on a third.  The
+        rebuild thus runs at the START of the step that needs it (the same decision, on the
+        same positions, as the eager driver's end-of-step rebuild), so the momenta are final
+        after the kick and leave while the drift runs: a chunk's H2D in step k + 1 waits only
+        for the same chunk's D2H in step k, and only q's round trip is on the critical path.
+        No host round trip per step or per rebuild; the eager driver's trajectory bit for bit,
+        except that a rebuild due after the last step is left to the next launch (the host
+        arrays then hold the state as of before it).  The momenta's pad lane (atom ids) is not
+        carried through the host arrays."""
+        if self.world != 1 or self.push or self.halo or not hasattr(self.be, "builder"):
+            raise ValueError("graph_host_io: one rank, liblj backend, all-gather exchange")
+        n = self.n
+        for t, name in ((q_host, "q_host"), (p_host, "p_host")):
+            if t.shape != (n, 3) or t.dtype != torch.float64 or not t.is_contiguous() or not t.is_pinned():
+                raise ValueError(f"graph_host_io: {name} must be a pinned contiguous (n, 3) float64 tensor")
+        torch.cuda.current_stream().synchronize()
+        self._resolve()
+        if hasattr(self.be, "headroom_ok") and not self.be.headroom_ok():
+            raise lj.LJError(lj.LJ_ERR_UNSUPPORTED, "graph: list rows within %d entries of the padded stride; "
+                             "use eager steps" % self.be.ROW_MARGIN)
+        dev = self.q.device
+        status = torch.zeros(4, dtype=torch.int64, device=dev)
+        rs = None
+        if self.reorder:
+            if getattr(self, "q_alt", None) is None:
+                self.q_alt = self.be.empty_records(n)
+            if getattr(self, "p_alt", None) is None:
+                self.p_alt = self.be.empty_records(n)
+            if getattr(self.be, "perm", None) is None:
+                self.be.perm = torch.empty(n, dtype=torch.int64, device=dev)
+            self._p_table = torch.tensor([self.p.data_ptr()], dtype=torch.int64, device=dev)
+            rs = dict(q_alt=self.q_alt, p=self.p, p_alt=self.p_alt, perm=self.be.perm, p_peers=self._p_table,
+                      n_own=n)
+        K = max(1, min(int(chunks), n)) if n >= chunk_min_rows else 1   # (small systems: one chunk)
+        cb = [n * c // K for c in range(K + 1)]
+        sl = [slice(cb[c], cb[c + 1]) for c in range(K)]
+        q_in, p_in, q_out, p_out = (torch.empty((n, 3), dtype=torch.float64, device=dev) for _ in range(4))
+        self._host_io = (q_host, p_host, q_in, p_in, q_out, p_out, status)   # the graph holds their pointers
+        g = torch.cuda.CUDAGraph()
+        cs, ci, cop, coq = (torch.cuda.Stream(device=dev) for _ in range(4))
+        cs.wait_stream(torch.cuda.current_stream())
+        l0 = lj.launch_count()
+        kpr = 0
+        with torch.cuda.graph(g, stream=cs, capture_error_mode="relaxed"):
+            # the first decision reads the current displacement (0 right after a rebuild)
+            self.be.max_disp(self.q, self.q_ref, 0, n, self.disp)
+            start = cs.record_event()
+            for st in (ci, cop, coq):
+                st.wait_event(start)
+            ev_qo, ev_po = [None] * K, [None] * K
+            for _ in range(steps):
+                ev_qi, ev_pi = [], []
+                with torch.cuda.stream(ci):   # p first: it left first in the previous step
+                    for c in range(K):
+                        if ev_po[c] is not None:
+                            ci.wait_event(ev_po[c])
+                        lj.copy_bytes(p_in[sl[c]], p_host[sl[c]])
+                        ev_pi.append(ci.record_event())
+                    for c in range(K):
+                        if ev_qo[c] is not None:
+                            ci.wait_event(ev_qo[c])
+                        lj.copy_bytes(q_in[sl[c]], q_host[sl[c]])
+                        ev_qi.append(ci.record_event())
+                for c in range(K):
+                    cs.wait_event(ev_pi[c])
+                    lj.pack_aos4(p_in[sl[c]], out=self.p[sl[c]])
+                for c in range(K):
+                    cs.wait_event(ev_qi[c])
+                    lj.pack_aos4(q_in[sl[c]], out=self.q[sl[c]])
+                kpr = lj.md_capture_rebuild(self.q, self.q_ref, self.g, self.be.builder, self.disp, 1, 0, status, rs)
+                for c in range(K):   # the kick per chunk; its momenta leave at once
+                    if K == 1:
+                        self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
+                    else:
+                        self.be.force_rows(self.q, self.p, self.dt, self.lst, cb[c], cb[c + 1], self.counter)
+                    lj.unpack_aos4(self.p[sl[c]], out=p_out[sl[c]])
+                    e_p = cs.record_event()
+                    with torch.cuda.stream(cop):
+                        cop.wait_event(e_p)
+                        lj.copy_bytes(p_host[sl[c]], p_out[sl[c]])
+                        ev_po[c] = cop.record_event()
+                self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, 0, n, self.disp)
+                lj.unpack_aos4(self.q, out=q_out)
+                e_q = cs.record_event()
+                with torch.cuda.stream(coq):
+                    coq.wait_event(e_q)
+                    for c in range(K):
+                        lj.copy_bytes(q_host[sl[c]], q_out[sl[c]])
+                        ev_qo[c] = coq.record_event()
+            for st in (ci, cop, coq):
+                cs.wait_event(st.record_event())
+        torch.cuda.current_stream().wait_stream(cs)
+        per_step_total = lj.launch_count() - l0 - kpr * steps
+        return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr), status)
+
     def _open_momentum_shares(self):
         """Two share buffers for the own momenta and, per buffer, a device table of every rank's
         buffer pointer (CUDA IPC mappings of the peers' buffers; this rank's own pointer locally)."""

@@ -94,6 +94,48 @@ def test_step_graph_equals_eager_steps(md, reorder):
     gr.close()
 
 
+def _eager_steps_ending_without_rebuild(sim, dt, k_min):
+    """Eager steps until at least k_min are done and the last one did not rebuild (the
+    end-to-end graph leaves a rebuild due after its last step to its next launch)."""
+    k = 0
+    while True:
+        r0 = sim.stats.rebuilds
+        sim.kick(dt, sim.counter)
+        sim.drift_and_exchange()
+        k += 1
+        if k >= k_min and sim.stats.rebuilds == r0:
+            return k
+
+
+@pytest.mark.parametrize("reorder,chunks", [(True, 4), (True, 1), (False, 3)])
+def test_graph_host_io_equals_eager_steps(md, reorder, chunks):
+    """LeapfrogMD.graph_host_io (bench.py's end-to-end path: the state copied from and back
+    into pinned host arrays every step, inside one CUDA graph with the device-side rebuild
+    decision, the rebuild at the start of the step that needs it) follows the eager driver's
+    trajectory bit for bit; the host arrays hold the state; a second launch continues it."""
+    from paper_1806_05713_b200 import lj
+    w = lj_inputs.make_system(10, jitter_seed=1, T=1.0, mom_seed=5, dt=0.01)
+    g = lj.geom(w.L, w.rc, w.rs)
+    dev = torch.device("cuda:0")
+    a, b = (md.LeapfrogMD(md.LibBackend(w.n, g, 0, w.n, dev), w.q, w.p, g, w.dt, reorder=reorder) for _ in range(2))
+    qh = torch.empty((w.n, 3), dtype=torch.float64, pin_memory=True)
+    ph = torch.empty((w.n, 3), dtype=torch.float64, pin_memory=True)
+    qh.copy_(b.q[:, :3])
+    ph.copy_(b.p[:, :3])
+    for rnd in range(2):
+        steps = _eager_steps_ending_without_rebuild(a, w.dt, 25)
+        r_before = b.stats.rebuilds
+        gr = b.graph_host_io(steps, qh, ph, chunks=chunks, chunk_min_rows=0)
+        gr.launch()
+        torch.cuda.synchronize()
+        gr.finish()
+        gr.close()
+        assert a.stats.rebuilds >= 3 * (rnd + 1) and b.stats.rebuilds == a.stats.rebuilds, (rnd, r_before)
+        assert torch.equal(a.q[:, :3].cpu(), qh) and torch.equal(a.p[:, :3].cpu(), ph), rnd
+        assert torch.equal(a.q[:, :3], b.q[:, :3]) and torch.equal(a.p[:, :3], b.p[:, :3]), rnd
+        assert a.interactions() == b.interactions(), rnd
+
+
 def test_step_graph_energy_samples(md):
     """energy_every: the graph splits the kick around lj_energy at sample steps, as the
     eager driver's bench path does -- same trajectory bit for bit, same energies."""
