@@ -654,7 +654,7 @@ class LeapfrogMD:
         into the records (lj_pack_aos4); the device-side bookkeeping decision on the previous
         drift's displacement with the conditional re-sorting rebuild (lj_md_capture_rebuild);
         the kick per row chunk, each chunk's momenta unpacked and sent back (D2H) at once on a
-        second copy stream; the drift + displacement; q unpacked and sent back on a third.  The
+        second copy stream; the drift + displacement; q unpacked and sent back after them.  The
         rebuild thus runs at the START of the step that needs it (the same decision, on the
         same positions, as the eager driver's end-of-step rebuild), so the momenta are final
         after the kick and leave while the drift runs: a chunk's H2D in step k + 1 waits only
@@ -693,7 +693,10 @@ class LeapfrogMD:
         q_in, p_in, q_out, p_out = (torch.empty((n, 3), dtype=torch.float64, device=dev) for _ in range(4))
         self._host_io = (q_host, p_host, q_in, p_in, q_out, p_out, status)   # the graph holds their pointers
         g = torch.cuda.CUDAGraph()
-        cs, ci, cop, coq = (torch.cuda.Stream(device=dev) for _ in range(4))
+        # one H2D and one D2H copy stream: on each, a step's momenta chunks precede its positions
+        # (they are final first), so q's copies -- the critical path -- never share the link
+        cs, ci, co = (torch.cuda.Stream(device=dev) for _ in range(3))
+        cop = coq = co
         cs.wait_stream(torch.cuda.current_stream())
         l0 = lj.launch_count()
         kpr = 0
@@ -701,7 +704,7 @@ class LeapfrogMD:
             # the first decision reads the current displacement (0 right after a rebuild)
             self.be.max_disp(self.q, self.q_ref, 0, n, self.disp)
             start = cs.record_event()
-            for st in (ci, cop, coq):
+            for st in (ci, co):
                 st.wait_event(start)
             ev_qo, ev_po = [None] * K, [None] * K
             for _ in range(steps):
@@ -743,7 +746,7 @@ class LeapfrogMD:
                     for c in range(K):
                         lj.copy_bytes(q_host[sl[c]], q_out[sl[c]])
                         ev_qo[c] = coq.record_event()
-            for st in (ci, cop, coq):
+            for st in (ci, co):
                 cs.wait_event(st.record_event())
         torch.cuda.current_stream().wait_stream(cs)
         per_step_total = lj.launch_count() - l0 - kpr * steps
