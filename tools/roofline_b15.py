@@ -104,11 +104,13 @@ def main():
                 doc["half_red_replay"].append(r)
                 print(json.dumps(r), flush=True)
             del half, pr
-        lst = lj.ListBuilder(w.n, g, False, device=dev, padded=True).build(q)
-        E = lst.n_entries
-        for G, U, X in VARIANTS:
+        for il in (False, True):   # the row-major padded list and the interleaved one (the MD driver's)
+          lst = lj.ListBuilder(w.n, g, False, device=dev, padded=True, interleaved=il).build(q)
+          E = lst.n_entries
+          for G, U, X in VARIANTS:
             lanes = G | (U << 8) | X
-            rec = {"cfg": cfg, "order": "cell" if cfg in (3, 4) else "shuffled", "list": "full, padded",
+            rec = {"cfg": cfg, "order": "cell" if cfg in (3, 4) else "shuffled",
+                   "list": "full, padded" + (", interleaved" if il else ""),
                    "G": G, "U": U, "idxv": bool(X), "lanes_per_row": lanes, "entries": E}
             try:
                 rec["probe_ms"] = min(timeit(lambda: lj.gather_probe(q, lst, lanes, sink), reps=20)
@@ -123,15 +125,18 @@ def main():
                 rec["force_ms"] = None
             doc["gather_replay"].append(rec)
             print(json.dumps(rec), flush=True)
-        del q, p, lst
+          del lst
+        del q, p
         torch.cuda.empty_cache()
 
     best = {}
     for r in doc["gather_replay"]:
-        if r["probe_ms"] is not None and (r["cfg"] not in best or r["probe_ms"] < best[r["cfg"]]["probe_ms"]):
-            best[r["cfg"]] = r
-    doc["best_replay"] = {str(k): {"probe_ms": v["probe_ms"], "lanes_per_row": v["lanes_per_row"], "G": v["G"],
-                                   "U": v["U"], "idxv": v["idxv"], "entries": v["entries"]} for k, v in best.items()}
+        k = (r["cfg"], r["list"])
+        if r["probe_ms"] is not None and (k not in best or r["probe_ms"] < best[k]["probe_ms"]):
+            best[k] = r
+    doc["best_replay"] = {f"{k[0]} ({k[1]})": {"probe_ms": v["probe_ms"], "lanes_per_row": v["lanes_per_row"],
+                                               "G": v["G"], "U": v["U"], "idxv": v["idxv"], "entries": v["entries"]}
+                          for k, v in best.items()}
     with open(out_path, "w") as f:
         json.dump(doc, f, indent=1)
     print("wrote", out_path, flush=True)
