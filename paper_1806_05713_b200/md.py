@@ -646,7 +646,7 @@ class LeapfrogMD:
         return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr), status)
 
     def graph_host_io(self, steps: int, q_host: torch.Tensor, p_host: torch.Tensor, chunks: int = 8,
-                      chunk_min_rows: int = 1 << 20) -> "StepGraph":
+                      chunk_min_rows: int = 1 << 20, timeline: list | None = None) -> "StepGraph":
         """The next `steps` leapfrog steps as ONE CUDA graph in which the state round-trips
         through the caller's page-locked host arrays q_host / p_host ((n, 3) float64, storage
         order) every step -- the end-to-end measurement of bench.py, one rank.  Per step: the
@@ -662,7 +662,9 @@ class LeapfrogMD:
         No host round trip per step or per rebuild; the eager driver's trajectory bit for bit,
         except that a rebuild due after the last step is left to the next launch (the host
         arrays then hold the state as of before it).  The momenta's pad lane (atom ids) is not
-        carried through the host arrays."""
+        carried through the host arrays.  timeline (instrumentation): a list that receives, per step, a
+        dict of CUDA events recorded inside the graph at the phase boundaries (elapsed times
+        readable after a launch)."""
         if self.world != 1 or self.push or self.halo or not hasattr(self.be, "builder"):
             raise ValueError("graph_host_io: one rank, liblj backend, all-gather exchange")
         n = self.n
@@ -707,7 +709,18 @@ class LeapfrogMD:
             for st in (ci, co):
                 st.wait_event(start)
             ev_qo, ev_po = [None] * K, [None] * K
+
+            def mark(tl, name, st):
+                if tl is not None:
+                    e = torch.cuda.Event(enable_timing=True, external=True)
+                    e.record(st)
+                    tl[name] = e
+
             for _ in range(steps):
+                tl = {} if timeline is not None else None
+                if tl is not None:
+                    timeline.append(tl)
+                mark(tl, "start", cs)
                 ev_qi, ev_pi = [], []
                 with torch.cuda.stream(ci):   # p first: it left first in the previous step
                     for c in range(K):
@@ -715,18 +728,22 @@ class LeapfrogMD:
                             ci.wait_event(ev_po[c])
                         lj.copy_bytes(p_in[sl[c]], p_host[sl[c]])
                         ev_pi.append(ci.record_event())
+                    mark(tl, "p_h2d", ci)
                     for c in range(K):
                         if ev_qo[c] is not None:
                             ci.wait_event(ev_qo[c])
                         lj.copy_bytes(q_in[sl[c]], q_host[sl[c]])
                         ev_qi.append(ci.record_event())
+                    mark(tl, "q_h2d", ci)
                 for c in range(K):
                     cs.wait_event(ev_pi[c])
                     lj.pack_aos4(p_in[sl[c]], out=self.p[sl[c]])
                 for c in range(K):
                     cs.wait_event(ev_qi[c])
                     lj.pack_aos4(q_in[sl[c]], out=self.q[sl[c]])
+                mark(tl, "q_in", cs)
                 kpr = lj.md_capture_rebuild(self.q, self.q_ref, self.g, self.be.builder, self.disp, 1, 0, status, rs)
+                mark(tl, "rebuild", cs)
                 for c in range(K):   # the kick per chunk; its momenta leave at once
                     if K == 1:
                         self.be.force(self.q, self.p, self.dt, self.lst, self.counter)
@@ -738,14 +755,18 @@ class LeapfrogMD:
                         cop.wait_event(e_p)
                         lj.copy_bytes(p_host[sl[c]], p_out[sl[c]])
                         ev_po[c] = cop.record_event()
+                mark(tl, "kick", cs)
+                mark(tl, "p_out", cop)
                 self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, 0, n, self.disp)
                 lj.unpack_aos4(self.q, out=q_out)
                 e_q = cs.record_event()
+                mark(tl, "drift", cs)
                 with torch.cuda.stream(coq):
                     coq.wait_event(e_q)
                     for c in range(K):
                         lj.copy_bytes(q_host[sl[c]], q_out[sl[c]])
                         ev_qo[c] = coq.record_event()
+                    mark(tl, "q_out", coq)
             for st in (ci, co):
                 cs.wait_event(st.record_event())
         torch.cuda.current_stream().wait_stream(cs)
