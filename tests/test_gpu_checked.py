@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # every builder path, every force kernel family (default lanes, index vectors, the ordered,
 # half-cells and variant kernels), energy, and the step graphs -- a few minutes, not the full matrix
 SUBSET = ("list or ordered or overflow or deferred or padding or counterexample or step_graph or rebuild or "
-          "half_cells or variants_at or energy")
+          "half_cells or variants_at or energy or interleaved or host_io")
 NODES = ([f"tests/test_gpu_parity.py::test_force_parity[{lanes}-{half}-{cfg}]"
           for lanes in (0, 772, 66052) for half in (True, False) for cfg in (1, 3)]
          + [f"tests/test_gpu_cutoff.py::test_force_at_cutoff_edge[{half}-772]" for half in (False, True)])
