@@ -159,9 +159,10 @@ class LibBackend:
 class _TorchGraph:
     """A torch.cuda.CUDAGraph with the interface StepGraph expects of lj.MDGraph."""
 
-    def __init__(self, graph, steps, kernels_steps, kernels_rebuild):
+    def __init__(self, graph, steps, kernels_steps, kernels_rebuild, keep=()):
         self.graph, self.steps = graph, steps
         self._k = (kernels_steps, kernels_rebuild)
+        self._keep = keep   # the buffers whose device pointers the graph holds (alive as long as it)
 
     def launch(self):
         self.graph.replay()
@@ -174,6 +175,7 @@ class _TorchGraph:
 
     def close(self):
         self.graph = None
+        self._keep = ()
 
 
 @dataclasses.dataclass
@@ -643,7 +645,8 @@ class LeapfrogMD:
                                             4 * n_own, status, rs[k % 2] if resort else None)
         torch.cuda.current_stream().wait_stream(cs)
         per_step_total = lj.launch_count() - l0 - kpr * steps
-        return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr), status)
+        keep = (self._p_share, self._p_tables) if resort else ()
+        return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr, keep), status)
 
     def graph_host_io(self, steps: int, q_host: torch.Tensor, p_host: torch.Tensor, chunks: int = 8,
                       chunk_min_rows: int = 1 << 20, timeline: list | None = None) -> "StepGraph":
@@ -771,7 +774,7 @@ class LeapfrogMD:
                 cs.wait_event(st.record_event())
         torch.cuda.current_stream().wait_stream(cs)
         per_step_total = lj.launch_count() - l0 - kpr * steps
-        return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr), status)
+        return StepGraph(self, _TorchGraph(g, steps, per_step_total, kpr, self._host_io + (rs,)), status)
 
     def _open_momentum_shares(self):
         """Two share buffers for the own momenta and, per buffer, a device table of every rank's
