@@ -701,7 +701,6 @@ class LeapfrogMD:
         # one H2D and one D2H copy stream: on each, a step's momenta chunks precede its positions
         # (they are final first), so q's copies -- the critical path -- never share the link
         cs, ci, co = (torch.cuda.Stream(device=dev) for _ in range(3))
-        cop = coq = co
         cs.wait_stream(torch.cuda.current_stream())
         l0 = lj.launch_count()
         kpr = 0
@@ -754,22 +753,22 @@ class LeapfrogMD:
                         self.be.force_rows(self.q, self.p, self.dt, self.lst, cb[c], cb[c + 1], self.counter)
                     lj.unpack_aos4(self.p[sl[c]], out=p_out[sl[c]])
                     e_p = cs.record_event()
-                    with torch.cuda.stream(cop):
-                        cop.wait_event(e_p)
+                    with torch.cuda.stream(co):
+                        co.wait_event(e_p)
                         lj.copy_bytes(p_host[sl[c]], p_out[sl[c]])
-                        ev_po[c] = cop.record_event()
+                        ev_po[c] = co.record_event()
                 mark(tl, "kick", cs)
-                mark(tl, "p_out", cop)
+                mark(tl, "p_out", co)
                 self.be.integrate_disp(self.q, self.p, self.q_ref, self.dt, 0, n, self.disp)
                 lj.unpack_aos4(self.q, out=q_out)
                 e_q = cs.record_event()
                 mark(tl, "drift", cs)
-                with torch.cuda.stream(coq):
-                    coq.wait_event(e_q)
+                with torch.cuda.stream(co):
+                    co.wait_event(e_q)
                     for c in range(K):
                         lj.copy_bytes(q_host[sl[c]], q_out[sl[c]])
-                        ev_qo[c] = coq.record_event()
-                    mark(tl, "q_out", coq)
+                        ev_qo[c] = co.record_event()
+                    mark(tl, "q_out", co)
             for st in (ci, co):
                 cs.wait_event(st.record_event())
         torch.cuda.current_stream().wait_stream(cs)
