@@ -699,7 +699,7 @@ class LeapfrogMD:
         self._host_io = (q_host, p_host, q_in, p_in, q_out, p_out, status)   # the graph holds their pointers
         g = torch.cuda.CUDAGraph()
         # one H2D and one D2H copy stream: on each, a step's momenta chunks precede its positions
-        # (they are final first), so q's copies -- the critical path -- never share the link
+        # (they are final first); q's round trip is the critical path
         cs, ci, co = (torch.cuda.Stream(device=dev) for _ in range(3))
         cs.wait_stream(torch.cuda.current_stream())
         l0 = lj.launch_count()
