@@ -78,6 +78,23 @@ def test_validation_before_launch(L):
                             ctypes.c_void_p(256), ctypes.c_void_p(256), 0, 1, None, None)
     assert st == lj.LJ_ERR_UNSUPPORTED
     assert L.lj_wrap(None, None, 0, 0.0, None) == lj.LJ_ERR_ARG
+    # LJ_LIST_INTERLEAVED needs the padded layout; its capacity is counted in blocks of 8 rows
+    ws = ctypes.c_size_t()
+    assert L.lj_build_list_workspace(4000, g, ctypes.byref(ws)) == lj.LJ_OK
+    st = L.lj_build_list_ex(ctypes.c_void_p(256), 4000, g, 0, 0, 4000, lj.LJ_LIST_INTERLEAVED, ctypes.c_void_p(256), ctypes.c_void_p(256),
+                            ctypes.c_void_p(256), 1 << 30, ctypes.byref(ne), ctypes.c_void_p(256), ws.value, None)
+    assert st == lj.LJ_ERR_ARG and b"PADDED" in L.lj_last_error()
+    st = L.lj_build_list_ex(ctypes.c_void_p(256), 4000, g, 0, 0, 3999, lj.LJ_LIST_PADDED | lj.LJ_LIST_INTERLEAVED,
+                            ctypes.c_void_p(256), ctypes.c_void_p(256), ctypes.c_void_p(256), 3999 * 196,
+                            ctypes.byref(ne), ctypes.c_void_p(256), ws.value, None)
+    assert st == lj.LJ_ERR_CAPACITY and ne.value == 4000 * 196   # 3,999 rows -> 500 blocks of 8
+    st = L.lj_build_list_ex(ctypes.c_void_p(256), 4000, g, 0, 0, 3999, 8, ctypes.c_void_p(256),
+                            ctypes.c_void_p(256), ctypes.c_void_p(256), 1 << 30, ctypes.byref(ne),
+                            ctypes.c_void_p(256), ws.value, None)
+    assert st == lj.LJ_ERR_ARG and b"flags" in L.lj_last_error()
+    # lj_copy_bytes: null pointers with a non-zero size; zero bytes is a no-op
+    assert L.lj_copy_bytes(None, ctypes.c_void_p(256), 8, None) == lj.LJ_ERR_ARG
+    assert L.lj_copy_bytes(None, None, 0, None) == lj.LJ_OK
 
 
 def test_validation_of_the_step_entry_points(L):
